@@ -1,0 +1,171 @@
+/*
+ * include/cbct.h -- C ABI of the B200-native cone-beam projector pair (libcbct.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * cbctkit 0.1.0 (/root/reference/pkg/src/cbctkit).  The reference's hot path is
+ * two Numba kernels behind CbctOperator:
+ *
+ *   _project_kernel(vol, out, srcs, det00, ustep, vstep, nu, nv,
+ *                   lo0, lo1, lo2, p0, p1, p2, n0, n1, n2)          operator.py:190-206
+ *   _backproject_kernel(proj, out, srcs, det00, ustep, vstep, nu, nv,
+ *                   lo0, lo1, lo2, p0, p1, p2, n0, n1, n2,
+ *                   n_workers, mode)                               operator.py:209-233
+ *
+ * and the CGLS/LSQR/PSIRT vector updates in solvers.py:269-569.
+ *
+ * Two levels are exported:
+ *
+ *  1. Stateless reference-signature entry points (cbct_ref_project /
+ *     cbct_ref_backproject): host fp64 buffers in the reference layouts
+ *     (volume x-fastest (nz,ny,nx); projections u-fastest (V,nv,nu)), the same
+ *     argument list as the Numba kernels.  They build (and cache) a plan, copy
+ *     in, run the CUDA kernels, copy out.  This is what a ctypes/cffi binding of
+ *     the reference would call in place of the Numba kernels.
+ *
+ *  2. The plan API used by the Python package: a cbct_plan owns the
+ *     device-resident fan-beam tables of one (volume, trajectory) pair and all
+ *     kernels run on caller-provided device buffers (torch-owned) in the
+ *     internal layouts:
+ *        volume:      [ny][nx][nz + 2*CBCT_ZPAD] fp32, z fastest, zero guard slices
+ *        projections: [n_views][nu][nv] fp32, v (detector row) fastest
+ *     Launches are asynchronous on the given stream, never allocate, and are
+ *     deterministic (no atomics on data).
+ *
+ * Every function returns 0 on success or a positive cudaError_t / negative
+ * CBCT_E* code; nothing throws across the ABI.  cbct_last_error() returns a
+ * message for the last failure on the calling thread.
+ */
+#ifndef CBCT_H
+#define CBCT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBCT_ZPAD 4 /* zero guard slices on each side of z in the internal volume layout */
+
+enum {
+    CBCT_OK = 0,
+    CBCT_E_ARG = -1,       /* invalid argument */
+    CBCT_E_GEOMETRY = -2,  /* geometry outside the supported family */
+    CBCT_E_NOMEM = -3,     /* device allocation failed */
+    CBCT_E_NODEVICE = -4,  /* no CUDA device */
+};
+
+/* Geometry of one operator, host memory.  Mirrors CbctOperator's inputs
+ * (operator.py:292-314): the per-view tables are those of _view_tables
+ * (operator.py:262-281), [n_views][3] fp64 each. */
+typedef struct cbct_geometry {
+    int64_t nx, ny, nz;        /* VolumeGeometry counts (geometry.py:44-46) */
+    double lo[3];              /* VolumeGeometry.corner() (geometry.py:69-74) */
+    double pitch[3];           /* voxel_size */
+    int64_t nu, nv, n_views;   /* DetectorGeometry nu, nv; TrajectoryGeometry n_views */
+    const double* srcs;        /* source_position per view */
+    const double* det00;       /* centre of pixel (0,0) per view */
+    const double* ustep;       /* pu * u_axis per view */
+    const double* vstep;       /* pv * v_axis per view */
+} cbct_geometry;
+
+typedef struct cbct_plan cbct_plan;
+
+/* Static facts about a plan (sizes of the internal layouts and of the tables). */
+typedef struct cbct_plan_info {
+    int64_t n_voxels;          /* nx*ny*nz */
+    int64_t n_rays;            /* n_views*nu*nv */
+    int64_t vol_elems;         /* padded internal volume length: ny*nx*(nz+2*CBCT_ZPAD) */
+    int64_t zstride;           /* nz + 2*CBCT_ZPAD */
+    int64_t n_columns;         /* n_views*nu detector columns */
+    int64_t n_intervals;       /* column/cell intersections = nnz of the 2-D fan-beam matrix */
+    int64_t max_intervals;     /* longest column list */
+    int64_t max_cell_entries;  /* longest cell list */
+    int64_t table_bytes;       /* device bytes held by the plan */
+    int32_t proj_blocks;       /* number of fp64 partials written by cbct_project */
+    int32_t bp_blocks;         /* number of fp64 partials written by cbct_backproject */
+} cbct_plan_info;
+
+/* ---- plan lifecycle ------------------------------------------------------ */
+/* Build the fan-beam tables on the current CUDA device (synchronous).
+ * Replaces CbctOperator.__init__'s table setup (operator.py:292-301). */
+int cbct_plan_create(cbct_plan** plan, const cbct_geometry* geom, void* stream);
+int cbct_plan_destroy(cbct_plan* plan);
+int cbct_plan_get_info(const cbct_plan* plan, cbct_plan_info* info);
+
+/* ---- operators on device buffers (internal layouts) ----------------------- */
+/* proj = A vol  (operator.py:190-206, 316-326).  If norm2_partials != NULL, it
+ * receives info.proj_blocks fp64 partial sums of proj^2 (reduce with
+ * cbct_reduce_partials).  All m entries of proj are written. */
+int cbct_project(const cbct_plan* plan, const float* vol, float* proj, double* norm2_partials,
+                 void* stream);
+
+/* vol = A^T proj (mode 1, operator.py:328-341) or diag(A^T A) (mode 2,
+ * operator.py:353-362; proj is ignored and may be NULL).  Every entry of vol,
+ * guards included, is written (guards with 0).  scratch_proj: n_rays fp32 device
+ * workspace (ray-length-weighted copy of proj).  If norm2_partials != NULL it
+ * receives info.bp_blocks fp64 partials of vol^2.  If col_scale != NULL the
+ * result is multiplied by col_scale (Jacobi chain applyT, solvers.py:178-181). */
+int cbct_backproject(const cbct_plan* plan, const float* proj, float* vol, int mode, float* scratch_proj,
+                     const float* col_scale, double* norm2_partials, void* stream);
+
+/* ---- layout conversion (reference layout <-> internal layout) ------------ */
+/* src: fp64 or fp32 (src_is_f64) reference-layout volume (nz,ny,nx) -> internal. */
+int cbct_volume_to_internal(const cbct_plan* plan, const void* src, int src_is_f64, float* dst, void* stream);
+/* internal -> fp64 or fp32 (dst_is_f64) reference layout (nz,ny,nx). */
+int cbct_volume_from_internal(const cbct_plan* plan, const float* src, void* dst, int dst_is_f64, void* stream);
+int cbct_proj_to_internal(const cbct_plan* plan, const void* src, int src_is_f64, float* dst, void* stream);
+int cbct_proj_from_internal(const cbct_plan* plan, const float* src, void* dst, int dst_is_f64, void* stream);
+
+/* ---- fused solver vector kernels (deterministic fp64 partials) ----------- */
+/* Vector kernels work on flat fp32 device vectors of length n (a padded
+ * internal volume or an internal projection set).  Kernels that reduce write
+ * cbct_vec_blocks(n) fp64 partials (fixed element->thread map); sum them with
+ * cbct_reduce_partials.  Scalars are fp64 host values, as in solvers.py. */
+int cbct_vec_blocks(int64_t n);
+/* CGLS volume update (solvers.py:345-346, 352; x-update deferred one iteration
+ * so both fuse into one 20 B/voxel pass):  if do_x: x += alpha_prev*d ;  d = r + beta*d */
+int cbct_cgls_volume_update(int64_t n, float* x, float* d, const float* r, double alpha_prev, int do_x,
+                            double beta, void* stream);
+/* CGLS projection update (solvers.py:353-355): e -= alpha*p, partials of e^2 (12 B/ray). */
+int cbct_cgls_proj_update(int64_t n, float* e, const float* p, double alpha, double* partials, void* stream);
+/* y = a*x + b*y (x NULL: y = b*y); partials of y^2 if partials != NULL. */
+int cbct_axpby(int64_t n, double a, const float* x, double b, float* y, double* partials, void* stream);
+/* out = a - b; partials of out^2 if partials != NULL. */
+int cbct_sub(int64_t n, const float* a, const float* b, float* out, double* partials, void* stream);
+/* partials of x . y */
+int cbct_dot(int64_t n, const float* x, const float* y, double* partials, void* stream);
+/* Deterministic fixed-order sum of n fp64 partials into *dev_out; if host_out is
+ * not NULL the result is also copied there (synchronising the stream). */
+int cbct_reduce_partials(const double* partials, int32_t n, double* dev_out, double* host_out, void* stream);
+
+/* Elementwise helpers on fp32 device vectors. */
+int cbct_mul(int64_t n, const float* a, const float* b, float* out, void* stream);       /* out = a*b */
+int cbct_clip(const cbct_plan* plan, float* vol, float lo, float hi, void* stream);     /* interior only */
+int cbct_fill(int64_t n, float* x, float value, void* stream);
+/* Fill a volume's interior with value and its guard slices with 0. */
+int cbct_fill_volume(const cbct_plan* plan, float* vol, float value, void* stream);
+
+/* ---- reference-signature entry points (host fp64, reference layouts) ------ */
+/* Drop-in for _project_kernel (operator.py:190-206). */
+int cbct_ref_project(const double* vol, double* out, const double* srcs, const double* det00,
+                     const double* ustep, const double* vstep, int64_t n_views, int64_t nu, int64_t nv,
+                     double lo0, double lo1, double lo2, double p0, double p1, double p2, int64_t n0,
+                     int64_t n1, int64_t n2);
+/* Drop-in for _backproject_kernel (operator.py:209-233): out += A^T proj (mode 1)
+ * or diag(A^T A) (mode 2).  n_workers is accepted for signature parity; the CUDA
+ * gather is deterministic for any value. */
+int cbct_ref_backproject(const double* proj, double* out, const double* srcs, const double* det00,
+                         const double* ustep, const double* vstep, int64_t n_views, int64_t nu, int64_t nv,
+                         double lo0, double lo1, double lo2, double p0, double p1, double p2, int64_t n0,
+                         int64_t n1, int64_t n2, int64_t n_workers, int mode);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+const char* cbct_last_error(void);
+int cbct_version(void);
+/* Number of kernel launches issued by this library since load (for the bench's gpu_launches). */
+int64_t cbct_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBCT_H */

@@ -1,0 +1,68 @@
+// cbct_internal.cuh -- private types and helpers of libcbct.so (sm_100a).
+//
+// Data layout in HBM:
+//   volume      [ny][nx][zs]   fp32, zs = nz + 2*CBCT_ZPAD, z fastest; slices
+//                              [0,ZPAD) and [ZPAD+nz, zs) are zero guards
+//   projections [V][nu][nv]    fp32, detector row v fastest
+//   column table (A):    per detector column c = view*nu + u, entries
+//                        [col_off[c], col_off[c+1]) of {tau_end fp32, cell_base int32}
+//   cell table   (A^T):  per cell (iy*nx+ix), entries [cell_off[k], cell_off[k+1])
+//                        of {vu int32, tau_a fp32, tau_b fp32}
+// tau = t - t_ref(column): ray parameter relative to a per-column anchor, which
+// keeps fp32 interval ends accurate to ~1e-8 of the ray (hard part 1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cbct.h"
+
+#define CBCT_CHECK(expr)                                       \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return cbct_fail_cuda(_e, #expr); \
+    } while (0)
+
+int cbct_fail_cuda(cudaError_t e, const char* what);
+int cbct_fail(int code, const char* msg);
+void cbct_count_launch(int n = 1);
+
+struct ColumnHeader {  // one detector column (view, u); fp64 facts from the plan builder
+    double tmin, tmax;  // xy box clip of the column's rays (operator.py:60-100), within [0,1]
+    double rxy2;        // rx^2 + ry^2
+    float t_ref;        // anchor, exactly representable in fp32
+    float tau_start;    // tmin - t_ref
+    int32_t flat_slab;  // z slab of a flat (|rz| < 1e-12 p2) ray in this column, or INT32_MIN
+    int32_t pad;
+};
+
+struct CellEntry {  // one column crossing a cell, in cell-major order
+    int32_t vu;
+    float tau_a, tau_b;
+};
+
+struct cbct_plan {
+    // geometry (host copies)
+    int64_t nx, ny, nz, zs;
+    double lo[3], pitch[3];
+    int64_t nu, nv, V;
+    double det00z, pv;  // detector row geometry shared by all views (v_axis = +z)
+    int32_t flat_v;     // index of the flat row (|w| < 1e-12 p2) or -1
+    // sizes
+    int64_t n_cols, n_cells, n_intervals, max_intervals, max_cell_entries;
+    int64_t vol_elems, n_rays;
+    size_t table_bytes;
+    // device tables
+    ColumnHeader* d_cols = nullptr;
+    int64_t* d_col_off = nullptr;   // n_cols + 1
+    float2* d_col_ent = nullptr;    // {tau_end, __int_as_float(cell_base)} n_intervals
+    int64_t* d_cell_off = nullptr;  // n_cells + 1
+    CellEntry* d_cell_ent = nullptr;
+    double* d_w = nullptr;          // per-row rz (fp64), nv
+    float* d_invw = nullptr;        // per-row 1/rz (fp32; +-1e30 for flat rows), nv
+    // launch shapes
+    int proj_threads, proj_rpt;
+    int bp_threads, bp_zpt;
+    int32_t proj_blocks, bp_blocks;
+};
+
+__device__ __forceinline__ int floor_to_int(double x) { return (int)floor(x); }

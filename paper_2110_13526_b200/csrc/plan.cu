@@ -1,0 +1,412 @@
+// plan.cu -- builds the device-resident 2-D fan-beam tables of one operator.
+//
+// Geometry facts used (all hold for every trajectory the reference can build,
+// geometry.py:144-164): the source is at z = 0, the detector v axis is +z and
+// the u axis is horizontal.  Hence every ray of a detector column (view, u)
+// shares (rx, ry): the column's rays all lie in one vertical plane and cross
+// the same sequence of (ix, iy) cells at the same ray parameters t.  Only the
+// z walk differs from ray to ray (rz = det00z + v*pv).
+//
+// The xy walk below restates the x/y part of _traverse (operator.py:60-186)
+// in fp64: same box clip, same axis-parallel rule (|r| < 1e-12 * pitch), same
+// clamped entry cell, same incremental plane parameters and tie order.  It
+// runs once per operator; the projector and backprojector then stream the
+// resulting fp32 tables.
+#include <cub/cub.cuh>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "cbct_internal.cuh"
+
+namespace {
+
+struct GeomDev {
+    double lo0, lo1, p0, p1;
+    int64_t nx, ny, nu, zs;
+};
+
+// Walk the xy part of one column.  Calls emit(tau_end_double, ix, iy) for every
+// interval of non-zero length; returns the number of intervals.
+template <typename Emit>
+__device__ int64_t walk_column(const GeomDev& g, double sx, double sy, double rx, double ry, double tmin,
+                               double tmax, Emit emit) {
+    int64_t ix = (int64_t)floor((sx + tmin * rx - g.lo0) / g.p0);  // operator.py:105-111
+    int64_t iy = (int64_t)floor((sy + tmin * ry - g.lo1) / g.p1);
+    if (ix < 0) ix = 0; else if (ix >= g.nx) ix = g.nx - 1;
+    if (iy < 0) iy = 0; else if (iy >= g.ny) iy = g.ny - 1;
+    const double big = 1e300;
+    double tx, ty, dtx, dty;
+    int stx, sty;
+    if (fabs(rx) < 1e-12 * g.p0) { tx = big; dtx = big; stx = 0; }  // operator.py:122-130
+    else {
+        stx = rx > 0 ? 1 : -1;
+        const double plane = g.lo0 + (double)(ix + (stx > 0 ? 1 : 0)) * g.p0;
+        tx = (plane - sx) / rx;
+        dtx = g.p0 / fabs(rx);
+    }
+    if (fabs(ry) < 1e-12 * g.p1) { ty = big; dty = big; sty = 0; }
+    else {
+        sty = ry > 0 ? 1 : -1;
+        const double plane = g.lo1 + (double)(iy + (sty > 0 ? 1 : 0)) * g.p1;
+        ty = (plane - sy) / ry;
+        dty = g.p1 / fabs(ry);
+    }
+    double t = tmin;
+    int64_t count = 0;
+    for (;;) {  // operator.py:152-186, x before y on ties
+        const double tn = ty < tx ? ty : tx;
+        const double te = tn < tmax ? tn : tmax;
+        if (te > t) { emit(te, ix, iy); ++count; }
+        if (tn >= tmax) break;
+        t = tn;
+        if (tx <= ty) {
+            ix += stx;
+            if (ix < 0 || ix >= g.nx) break;
+            tx += dtx;
+        } else {
+            iy += sty;
+            if (iy < 0 || iy >= g.ny) break;
+            ty += dty;
+        }
+    }
+    return count;
+}
+
+// Column geometry: (sx, sy, rx, ry) exactly as operator.py:200-204 forms them
+// (no FMA contraction: the pixel position is det00 + u*ustep + v*vstep with
+// vstep_xy = 0).
+__device__ void column_ray(const double* srcs, const double* det00, const double* ustep, int64_t view, int64_t u,
+                           double& sx, double& sy, double& rx, double& ry) {
+    sx = srcs[view * 3 + 0];
+    sy = srcs[view * 3 + 1];
+    const double px = __dadd_rn(det00[view * 3 + 0], __dmul_rn((double)u, ustep[view * 3 + 0]));
+    const double py = __dadd_rn(det00[view * 3 + 1], __dmul_rn((double)u, ustep[view * 3 + 1]));
+    rx = __dsub_rn(px, sx);
+    ry = __dsub_rn(py, sy);
+}
+
+// operator.py:62-86 (x and y clips only; z is per ray).
+__device__ bool clip_xy(const GeomDev& g, double sx, double sy, double rx, double ry, double& tmin, double& tmax) {
+    tmin = 0.0;
+    tmax = 1.0;
+    double t1, t2, tt;
+    if (fabs(rx) < 1e-12 * g.p0) {
+        if (sx < g.lo0 || sx >= g.lo0 + (double)g.nx * g.p0) return false;
+    } else {
+        t1 = (g.lo0 - sx) / rx;
+        t2 = (g.lo0 + (double)g.nx * g.p0 - sx) / rx;
+        if (t1 > t2) { tt = t1; t1 = t2; t2 = tt; }
+        if (t1 > tmin) tmin = t1;
+        if (t2 < tmax) tmax = t2;
+    }
+    if (fabs(ry) < 1e-12 * g.p1) {
+        if (sy < g.lo1 || sy >= g.lo1 + (double)g.ny * g.p1) return false;
+    } else {
+        t1 = (g.lo1 - sy) / ry;
+        t2 = (g.lo1 + (double)g.ny * g.p1 - sy) / ry;
+        if (t1 > t2) { tt = t1; t1 = t2; t2 = tt; }
+        if (t1 > tmin) tmin = t1;
+        if (t2 < tmax) tmax = t2;
+    }
+    return tmax > tmin;
+}
+
+__global__ void k_column_headers(GeomDev g, const double* srcs, const double* det00, const double* ustep,
+                                 int64_t n_cols, double flat_w, int flat_v, double lo2, double p2, int64_t nz,
+                                 ColumnHeader* cols, int64_t* counts) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    const int64_t view = c / g.nu, u = c - view * g.nu;
+    double sx, sy, rx, ry, tmin, tmax;
+    column_ray(srcs, det00, ustep, view, u, sx, sy, rx, ry);
+    ColumnHeader h;
+    h.rxy2 = rx * rx + ry * ry;
+    h.flat_slab = INT_MIN;
+    h.pad = 0;
+    int64_t n = 0;
+    if (clip_xy(g, sx, sy, rx, ry, tmin, tmax)) {
+        h.tmin = tmin;
+        h.tmax = tmax;
+        h.t_ref = (float)(0.5 * (tmin + tmax));
+        h.tau_start = (float)(tmin - (double)h.t_ref);
+        n = walk_column(g, sx, sy, rx, ry, tmin, tmax, [](double, int64_t, int64_t) {});
+        if (flat_v >= 0) {
+            // flat ray: z never changes; operator.py:87-89 inside test, 107 entry slab, 116-119 clamp
+            const double sz = 0.0;
+            if (!(sz < lo2 || sz >= lo2 + (double)nz * p2)) {
+                int64_t iz = (int64_t)floor((sz + tmin * flat_w - lo2) / p2);
+                if (iz < 0) iz = 0; else if (iz >= nz) iz = nz - 1;
+                h.flat_slab = (int32_t)iz;
+            }
+        }
+    } else {
+        h.tmin = 0.0;
+        h.tmax = 0.0;
+        h.t_ref = 0.0f;
+        h.tau_start = 0.0f;
+    }
+    cols[c] = h;
+    counts[c] = n;
+}
+
+__global__ void k_column_fill(GeomDev g, const double* srcs, const double* det00, const double* ustep,
+                              int64_t n_cols, const ColumnHeader* cols, const int64_t* off, float2* ent,
+                              int32_t* cellkey, int32_t* colid) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    const ColumnHeader h = cols[c];
+    if (off[c + 1] == off[c]) return;
+    const int64_t view = c / g.nu, u = c - view * g.nu;
+    double sx, sy, rx, ry;
+    column_ray(srcs, det00, ustep, view, u, sx, sy, rx, ry);
+    int64_t k = off[c];
+    const double tref = (double)h.t_ref;
+    walk_column(g, sx, sy, rx, ry, h.tmin, h.tmax, [&](double te, int64_t ix, int64_t iy) {
+        const int64_t cell = iy * g.nx + ix;
+        ent[k] = make_float2((float)(te - tref), __int_as_float((int32_t)(cell * g.zs)));
+        cellkey[k] = (int32_t)cell;
+        colid[k] = (int32_t)c;
+        ++k;
+    });
+}
+
+__global__ void k_cell_entries(const int32_t* sorted_idx, int64_t n, const float2* ent, const int32_t* colid,
+                               const int64_t* col_off, const ColumnHeader* cols, CellEntry* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t e = (int64_t)(uint32_t)sorted_idx[k];
+    const int32_t c = colid[e];
+    CellEntry ce;
+    ce.vu = c;
+    ce.tau_b = ent[e].x;
+    ce.tau_a = (e == col_off[c]) ? cols[c].tau_start : ent[e - 1].x;
+    out[k] = ce;
+}
+
+__global__ void k_cell_offsets(const int32_t* sorted_keys, int64_t n, int64_t n_cells, int64_t* cell_off) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k > n_cells) return;
+    // lower_bound(sorted_keys, k)
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sorted_keys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    cell_off[k] = lo;
+}
+
+__global__ void k_max_span(const int64_t* off, int64_t n, unsigned long long* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    atomicMax(out, (unsigned long long)(off[k + 1] - off[k]));
+}
+
+__global__ void k_row_tables(int64_t nv, double det00z, double pv, double p2, double* w, float* invw) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    // operator.py:203 with ustep_z = 0, sz = 0: rz = (det00z + u*0.0) + v*pv
+    const double wv = __dadd_rn(det00z, __dmul_rn((double)v, pv));
+    w[v] = wv;
+    invw[v] = fabs(wv) < 1e-12 * p2 ? 1e30f : (float)(1.0 / wv);
+}
+
+__global__ void k_iota(int32_t* q, int64_t n) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) q[k] = (int32_t)(uint32_t)k;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+template <typename T>
+static int dev_alloc(T** p, size_t count, size_t* total) {
+    const size_t bytes = (count ? count : 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void**)p, bytes);
+    if (e != cudaSuccess) return cbct_fail(CBCT_E_NOMEM, "cudaMalloc failed while building the plan");
+    if (total) *total += bytes;
+    return 0;
+}
+
+extern "C" int cbct_plan_destroy(cbct_plan* p) {
+    if (!p) return 0;
+    cudaFree(p->d_cols);
+    cudaFree(p->d_col_off);
+    cudaFree(p->d_col_ent);
+    cudaFree(p->d_cell_off);
+    cudaFree(p->d_cell_ent);
+    cudaFree(p->d_w);
+    cudaFree(p->d_invw);
+    delete p;
+    return 0;
+}
+
+extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* stream_) {
+    if (!out || !g || !g->srcs || !g->det00 || !g->ustep || !g->vstep)
+        return cbct_fail(CBCT_E_ARG, "cbct_plan_create: null argument");
+    *out = nullptr;
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1 || g->nu < 1 || g->nv < 1 || g->n_views < 1)
+        return cbct_fail(CBCT_E_ARG, "cbct_plan_create: counts must be >= 1");
+    if (!(g->pitch[0] > 0 && g->pitch[1] > 0 && g->pitch[2] > 0))
+        return cbct_fail(CBCT_E_ARG, "cbct_plan_create: voxel pitch must be > 0");
+    const int64_t zs = g->nz + 2 * CBCT_ZPAD;
+    if (g->nx * g->ny * zs >= (int64_t)INT32_MAX)
+        return cbct_fail(CBCT_E_GEOMETRY, "volume too large for 32-bit cell offsets on one device");
+    const int64_t V = g->n_views;
+    // The circular-trajectory family (geometry.py:144-164): source z = 0, u axis
+    // horizontal, v axis = +z with one common pitch and one common det00 z.
+    const double det00z = g->det00[2], pv = g->vstep[2];
+    for (int64_t k = 0; k < V; ++k) {
+        if (g->srcs[k * 3 + 2] != 0.0 || g->ustep[k * 3 + 2] != 0.0 || g->vstep[k * 3 + 0] != 0.0 ||
+            g->vstep[k * 3 + 1] != 0.0 || g->vstep[k * 3 + 2] != pv || g->det00[k * 3 + 2] != det00z)
+            return cbct_fail(CBCT_E_GEOMETRY,
+                             "trajectory is not a circular orbit with a +z detector v axis (geometry.py:144-164)");
+    }
+    if (!(pv > 0)) return cbct_fail(CBCT_E_GEOMETRY, "detector v pitch must be > 0");
+    cudaStream_t stream = (cudaStream_t)stream_;
+
+    cbct_plan* p = new cbct_plan();
+    p->nx = g->nx; p->ny = g->ny; p->nz = g->nz; p->zs = zs;
+    for (int a = 0; a < 3; ++a) { p->lo[a] = g->lo[a]; p->pitch[a] = g->pitch[a]; }
+    p->nu = g->nu; p->nv = g->nv; p->V = V;
+    p->det00z = det00z; p->pv = pv;
+    p->flat_v = -1;
+    for (int64_t v = 0; v < g->nv; ++v) {
+        const double wv = det00z + (double)v * pv;  // k_row_tables' association
+        if (fabs(wv) < 1e-12 * g->pitch[2]) { p->flat_v = (int32_t)v; break; }
+    }
+    p->n_cols = V * g->nu;
+    p->n_cells = g->nx * g->ny;
+    p->vol_elems = p->n_cells * zs;
+    p->n_rays = p->n_cols * g->nv;
+    size_t total = 0;
+    int rc = 0;
+
+    double *d_srcs = nullptr, *d_det00 = nullptr, *d_ustep = nullptr;
+    int64_t* d_counts = nullptr;
+    int32_t *d_cellkey = nullptr, *d_colid = nullptr, *d_keys_sorted = nullptr, *d_idx = nullptr,
+            *d_idx_sorted = nullptr;
+    void* d_tmp = nullptr;
+    unsigned long long* d_max = nullptr;
+
+#define TRY(x) do { rc = (x); if (rc) goto fail; } while (0)
+#define TRYC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { rc = cbct_fail_cuda(_e, #x); goto fail; } } while (0)
+    {
+        const size_t tb = (size_t)V * 3 * sizeof(double);
+        TRY(dev_alloc(&d_srcs, V * 3, nullptr));
+        TRY(dev_alloc(&d_det00, V * 3, nullptr));
+        TRY(dev_alloc(&d_ustep, V * 3, nullptr));
+        TRYC(cudaMemcpyAsync(d_srcs, g->srcs, tb, cudaMemcpyHostToDevice, stream));
+        TRYC(cudaMemcpyAsync(d_det00, g->det00, tb, cudaMemcpyHostToDevice, stream));
+        TRYC(cudaMemcpyAsync(d_ustep, g->ustep, tb, cudaMemcpyHostToDevice, stream));
+
+        GeomDev gd{g->lo[0], g->lo[1], g->pitch[0], g->pitch[1], g->nx, g->ny, g->nu, zs};
+        TRY(dev_alloc(&p->d_cols, p->n_cols, &total));
+        TRY(dev_alloc(&p->d_col_off, p->n_cols + 1, &total));
+        TRY(dev_alloc(&d_counts, p->n_cols + 1, nullptr));
+        TRYC(cudaMemsetAsync(d_counts, 0, (p->n_cols + 1) * sizeof(int64_t), stream));
+        const double flat_w = p->flat_v >= 0 ? det00z + (double)p->flat_v * pv : 0.0;
+        k_column_headers<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(gd, d_srcs, d_det00, d_ustep, p->n_cols,
+                                                                         flat_w, p->flat_v, g->lo[2], g->pitch[2],
+                                                                         g->nz, p->d_cols, d_counts);
+        TRYC(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        TRYC(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_counts, p->d_col_off, p->n_cols + 1, stream));
+        TRYC(cudaMalloc(&d_tmp, tmp_bytes));
+        TRYC(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_counts, p->d_col_off, p->n_cols + 1, stream));
+        cudaFree(d_tmp); d_tmp = nullptr;
+        TRYC(cudaMemcpyAsync(&p->n_intervals, p->d_col_off + p->n_cols, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             stream));
+        TRYC(cudaStreamSynchronize(stream));
+        const int64_t n = p->n_intervals;
+        if (n >= (int64_t)UINT32_MAX) { rc = cbct_fail(CBCT_E_GEOMETRY, "too many fan-beam intervals"); goto fail; }
+
+        TRY(dev_alloc(&p->d_col_ent, n, &total));
+        TRY(dev_alloc(&d_cellkey, n, nullptr));
+        TRY(dev_alloc(&d_colid, n, nullptr));
+        k_column_fill<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(gd, d_srcs, d_det00, d_ustep, p->n_cols,
+                                                                      p->d_cols, p->d_col_off, p->d_col_ent,
+                                                                      d_cellkey, d_colid);
+        TRYC(cudaGetLastError());
+
+        // cell-major order: stable radix sort of entry indices by cell (keeps column order per cell)
+        TRY(dev_alloc(&d_idx, n, nullptr));
+        TRY(dev_alloc(&d_idx_sorted, n, nullptr));
+        TRY(dev_alloc(&d_keys_sorted, n, nullptr));
+        k_iota<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx, n);
+        TRYC(cudaGetLastError());
+        int end_bit = 1;
+        while ((int64_t(1) << end_bit) <= p->n_cells) ++end_bit;
+        tmp_bytes = 0;
+        TRYC(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                             (int64_t)n, 0, end_bit, stream));
+        TRYC(cudaMalloc(&d_tmp, tmp_bytes));
+        TRYC(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                             (int64_t)n, 0, end_bit, stream));
+        cudaFree(d_tmp); d_tmp = nullptr;
+
+        TRY(dev_alloc(&p->d_cell_ent, n, &total));
+        TRY(dev_alloc(&p->d_cell_off, p->n_cells + 1, &total));
+        k_cell_entries<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx_sorted, n, p->d_col_ent, d_colid,
+                                                               p->d_col_off, p->d_cols, p->d_cell_ent);
+        TRYC(cudaGetLastError());
+        k_cell_offsets<<<blocks_for(p->n_cells + 1, 256), 256, 0, stream>>>(d_keys_sorted, n, p->n_cells,
+                                                                            p->d_cell_off);
+        TRYC(cudaGetLastError());
+
+        TRY(dev_alloc(&d_max, 2, nullptr));
+        TRYC(cudaMemsetAsync(d_max, 0, 2 * sizeof(unsigned long long), stream));
+        k_max_span<<<blocks_for(p->n_cols, 256), 256, 0, stream>>>(p->d_col_off, p->n_cols, d_max);
+        k_max_span<<<blocks_for(p->n_cells, 256), 256, 0, stream>>>(p->d_cell_off, p->n_cells, d_max + 1);
+        unsigned long long mx[2];
+        TRYC(cudaMemcpyAsync(mx, d_max, sizeof(mx), cudaMemcpyDeviceToHost, stream));
+
+        TRY(dev_alloc(&p->d_w, g->nv, &total));
+        TRY(dev_alloc(&p->d_invw, g->nv, &total));
+        k_row_tables<<<blocks_for(g->nv, 128), 128, 0, stream>>>(g->nv, det00z, pv, g->pitch[2], p->d_w, p->d_invw);
+        TRYC(cudaGetLastError());
+        TRYC(cudaStreamSynchronize(stream));
+        p->max_intervals = (int64_t)mx[0];
+        p->max_cell_entries = (int64_t)mx[1];
+    }
+    cbct_count_launch(9);
+    // launch shapes (DESIGN.md 4.1 / 4.2)
+    p->proj_rpt = g->nv <= 512 ? 1 : (g->nv <= 1024 ? 2 : 4);
+    p->proj_threads = (int)(((g->nv + p->proj_rpt - 1) / p->proj_rpt + 31) / 32 * 32);
+    p->proj_blocks = (int32_t)p->n_cols;
+    p->bp_zpt = g->nz <= 512 ? 1 : (g->nz <= 1024 ? 2 : 4);
+    p->bp_threads = (int)(((g->nz + p->bp_zpt - 1) / p->bp_zpt + 31) / 32 * 32);
+    p->bp_blocks = (int32_t)p->n_cells;
+    p->table_bytes = total;
+    cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);
+    cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
+    *out = p;
+    return 0;
+fail:
+    cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);
+    cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
+    cudaFree(d_tmp);
+    cbct_plan_destroy(p);
+    return rc;
+#undef TRY
+#undef TRYC
+}
+
+extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
+    if (!p || !info) return cbct_fail(CBCT_E_ARG, "cbct_plan_get_info: null argument");
+    info->n_voxels = p->nx * p->ny * p->nz;
+    info->n_rays = p->n_rays;
+    info->vol_elems = p->vol_elems;
+    info->zstride = p->zs;
+    info->n_columns = p->n_cols;
+    info->n_intervals = p->n_intervals;
+    info->max_intervals = p->max_intervals;
+    info->max_cell_entries = p->max_cell_entries;
+    info->table_bytes = (int64_t)p->table_bytes;
+    info->proj_blocks = p->proj_blocks;
+    info->bp_blocks = p->bp_blocks;
+    return 0;
+}

@@ -1,0 +1,236 @@
+// vec.cu -- fused solver vector kernels (HBM-bound), deterministic fp64 partials.
+//
+// A CGLS iteration (solvers.py:339-357) is, besides A and A^T:
+//   volume:      x += alpha_prev*d ; d = r + beta*d        (x-update deferred one
+//                iteration so both fuse into one pass: 20 B/voxel)
+//   projection:  e -= alpha*p ; ||e||^2                    (12 B/ray)
+// ||r||^2 and ||p||^2 come from the A^T / A epilogues.  Every reduction writes one
+// fp64 partial per CTA with a fixed element->thread map, then cbct_reduce_partials
+// sums them in a fixed order, so results are bitwise reproducible.
+#include <cmath>
+
+#include "cbct_internal.cuh"
+#include "reduce.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 148 * 8;
+
+inline int vec_blocks(int64_t n) {
+    const int64_t b = (n + kThreads * 4 - 1) / (kThreads * 4);
+    return (int)(b < 1 ? 1 : (b > kMaxBlocks ? kMaxBlocks : b));
+}
+
+__device__ __forceinline__ void finish(double sq, double* partials) {
+    if (partials) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_cgls_volume(int64_t n, float* __restrict__ x, float* __restrict__ d, const float* __restrict__ r,
+                              float alpha_prev, int do_x, float beta, int use4) {
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* d4 = reinterpret_cast<float4*>(d);
+    const float4* r4 = reinterpret_cast<const float4*>(r);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 dv = d4[i];
+        const float4 rv = r4[i];
+        if (do_x) {
+            float4 xv = x4[i];
+            xv.x = fmaf(alpha_prev, dv.x, xv.x); xv.y = fmaf(alpha_prev, dv.y, xv.y);
+            xv.z = fmaf(alpha_prev, dv.z, xv.z); xv.w = fmaf(alpha_prev, dv.w, xv.w);
+            x4[i] = xv;
+        }
+        dv.x = fmaf(beta, dv.x, rv.x); dv.y = fmaf(beta, dv.y, rv.y);
+        dv.z = fmaf(beta, dv.z, rv.z); dv.w = fmaf(beta, dv.w, rv.w);
+        d4[i] = dv;
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (do_x) x[i] = fmaf(alpha_prev, d[i], x[i]);
+        d[i] = fmaf(beta, d[i], r[i]);
+    }
+}
+
+// y = a*x + b*y (x may be NULL: y = b*y); partials of y^2
+__global__ void k_axpby(int64_t n, float a, const float* __restrict__ x, float b, float* __restrict__ y,
+                        double* __restrict__ partials, int use4) {
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    float4* y4 = reinterpret_cast<float4*>(y);
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 yv = y4[i];
+        if (x) {
+            const float4 xv = x4[i];
+            yv.x = fmaf(a, xv.x, b * yv.x); yv.y = fmaf(a, xv.y, b * yv.y);
+            yv.z = fmaf(a, xv.z, b * yv.z); yv.w = fmaf(a, xv.w, b * yv.w);
+        } else {
+            yv.x *= b; yv.y *= b; yv.z *= b; yv.w *= b;
+        }
+        y4[i] = yv;
+        sq += (double)yv.x * yv.x + (double)yv.y * yv.y + (double)yv.z * yv.z + (double)yv.w * yv.w;
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float yv = x ? fmaf(a, x[i], b * y[i]) : b * y[i];
+        y[i] = yv;
+        sq += (double)yv * yv;
+    }
+    finish(sq, partials);
+}
+
+// out = a - b ; partials of out^2
+__global__ void k_sub(int64_t n, const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
+                      double* __restrict__ partials) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float v = a[i] - b[i];
+        out[i] = v;
+        sq += (double)v * v;
+    }
+    finish(sq, partials);
+}
+
+// partials of x.y
+__global__ void k_dot(int64_t n, const float* __restrict__ x, const float* __restrict__ y,
+                      double* __restrict__ partials) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        s += (double)x[i] * (double)y[i];
+    finish(s, partials);
+}
+
+__global__ void k_mul(int64_t n, const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ o) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) o[i] = a[i] * b[i];
+}
+
+__global__ void k_fill(int64_t n, float* __restrict__ x, float v) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) x[i] = v;
+}
+
+__global__ void k_fill_volume(int64_t n, int64_t zs, int64_t nz, float* __restrict__ x, float v) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t k = i % zs;
+        x[i] = (k >= CBCT_ZPAD && k < CBCT_ZPAD + nz) ? v : 0.0f;
+    }
+}
+
+__global__ void k_clip(int64_t n, int64_t zs, int64_t nz, float* __restrict__ x, float lo, float hi) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t k = i % zs;
+        if (k >= CBCT_ZPAD && k < CBCT_ZPAD + nz) x[i] = fminf(fmaxf(x[i], lo), hi);
+    }
+}
+
+__global__ void k_reduce(const double* __restrict__ partials, int n, double* __restrict__ out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
+    const double t = block_sum(s);
+    if (threadIdx.x == 0) *out = t;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+extern "C" int cbct_vec_blocks(int64_t n) { return vec_blocks(n); }
+
+extern "C" int cbct_cgls_volume_update(int64_t n, float* x, float* d, const float* r, double alpha_prev, int do_x,
+                                       double beta, void* stream) {
+    if (!d || !r || (do_x && !x)) return cbct_fail(CBCT_E_ARG, "cbct_cgls_volume_update: null argument");
+    const int use4 = aligned16(x) && aligned16(d) && aligned16(r);
+    k_cgls_volume<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, d, r, (float)alpha_prev, do_x,
+                                                                       (float)beta, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_axpby(int64_t n, double a, const float* x, double b, float* y, double* partials,
+                          void* stream) {
+    if (!y) return cbct_fail(CBCT_E_ARG, "cbct_axpby: null y");
+    const int use4 = aligned16(x) && aligned16(y);
+    k_axpby<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, (float)a, x, (float)b, y, partials, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_cgls_proj_update(int64_t n, float* e, const float* p, double alpha, double* partials,
+                                     void* stream) {
+    // e -= alpha*p  ==  axpby(-alpha, p, 1, e)
+    return cbct_axpby(n, -alpha, p, 1.0, e, partials, stream);
+}
+
+extern "C" int cbct_sub(int64_t n, const float* a, const float* b, float* out, double* partials, void* stream) {
+    if (!a || !b || !out) return cbct_fail(CBCT_E_ARG, "cbct_sub: null argument");
+    k_sub<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, a, b, out, partials);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_dot(int64_t n, const float* x, const float* y, double* partials, void* stream) {
+    if (!x || !y || !partials) return cbct_fail(CBCT_E_ARG, "cbct_dot: null argument");
+    k_dot<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, y, partials);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_mul(int64_t n, const float* a, const float* b, float* out, void* stream) {
+    if (!a || !b || !out) return cbct_fail(CBCT_E_ARG, "cbct_mul: null argument");
+    k_mul<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, a, b, out);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_fill(int64_t n, float* x, float value, void* stream) {
+    if (!x) return cbct_fail(CBCT_E_ARG, "cbct_fill: null argument");
+    k_fill<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, value);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_fill_volume(const cbct_plan* p, float* vol, float value, void* stream) {
+    if (!p || !vol) return cbct_fail(CBCT_E_ARG, "cbct_fill_volume: null argument");
+    k_fill_volume<<<vec_blocks(p->vol_elems), kThreads, 0, (cudaStream_t)stream>>>(p->vol_elems, p->zs, p->nz, vol,
+                                                                                   value);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_clip(const cbct_plan* p, float* vol, float lo, float hi, void* stream) {
+    if (!p || !vol) return cbct_fail(CBCT_E_ARG, "cbct_clip: null argument");
+    k_clip<<<vec_blocks(p->vol_elems), kThreads, 0, (cudaStream_t)stream>>>(p->vol_elems, p->zs, p->nz, vol, lo, hi);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_reduce_partials(const double* partials, int32_t n, double* dev_out, double* host_out,
+                                    void* stream) {
+    if (!partials || !dev_out || n < 1) return cbct_fail(CBCT_E_ARG, "cbct_reduce_partials: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    k_reduce<<<1, 1024, 0, s>>>(partials, n, dev_out);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    if (host_out) {
+        CBCT_CHECK(cudaMemcpyAsync(host_out, dev_out, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CBCT_CHECK(cudaStreamSynchronize(s));
+    }
+    return 0;
+}

@@ -1,0 +1,318 @@
+"""The system matrix A as a CUDA projector pair (API of cbctkit.operator).
+
+``CbctOperator`` is a drop-in for the reference's ``CbctOperator``
+(operator.py:284-374): same constructor, ``project``/``backproject``,
+``row_sums``/``col_sums``/``normal_diagonal``, ``ray_segments``, ``n``/``m``,
+``vol_geom``/``trajectory``/``workers``, ``GeometryMismatchError`` raised before
+any compute.  The work runs in libcbct.so (hand-written sm_100a CUDA, see
+``csrc/``) on fp32 device buffers; there is no CPU fallback.
+
+Containers passed in decide what comes back:
+
+* host numpy data (the reference's containers) -> fp64 numpy out, aliasing
+  ``out`` when given (operator.py:320-326, 332-341);
+* torch CUDA data in the reference layout -> fp32 torch out;
+* containers flagged ``internal=True`` hold the operator's device layout
+  (volume z-fastest with zero guard slices, projections v-fastest) and are
+  what the solvers iterate on: no layout conversion per call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import CBCT_ZPAD, call
+from .geometry import TrajectoryGeometry, VolumeGeometry, geometry_key, view_tables
+from .phantom import Volume, coerce_data
+
+__all__ = ["GeometryMismatchError", "ProjectionStack", "CbctOperator", "InternalVolume", "InternalProjections"]
+
+
+class GeometryMismatchError(ValueError):
+    """Input volume/projection geometry does not match the operator's."""
+
+
+@dataclass
+class ProjectionStack:
+    """Line integrals, flat u-fastest then v then view (operator.py:30-50)."""
+
+    trajectory: TrajectoryGeometry
+    data: object = field(default=None)
+
+    def __post_init__(self):
+        m = self.trajectory.n_rays
+        if self.data is None:
+            self.data = np.zeros(m, dtype=np.float64)
+        else:
+            self.data = coerce_data(self.data, m, "nu*nv*n_views")
+
+    def as_3d(self):
+        t = self.trajectory
+        return self.data.reshape(t.n_views, t.detector.nv, t.detector.nu)
+
+
+@dataclass
+class InternalVolume:
+    """A volume in the device layout [ny][nx][nz + 2*ZPAD] (fp32, zero guards)."""
+
+    geometry: VolumeGeometry
+    data: torch.Tensor
+    internal: bool = True
+
+    def as_3d(self):
+        g = self.geometry
+        zs = g.nz + 2 * CBCT_ZPAD
+        return self.data.view(g.ny, g.nx, zs)[:, :, CBCT_ZPAD:CBCT_ZPAD + g.nz].permute(2, 0, 1)
+
+
+@dataclass
+class InternalProjections:
+    """Projections in the device layout [n_views][nu][nv] (fp32)."""
+
+    trajectory: TrajectoryGeometry
+    data: torch.Tensor
+    internal: bool = True
+
+    def as_3d(self):
+        t = self.trajectory
+        return self.data.view(t.n_views, t.detector.nu, t.detector.nv).permute(0, 2, 1)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class CbctOperator:
+    """Matched Siddon projector pair on one CUDA device.
+
+    Immutable after construction.  ``workers`` is kept for API parity
+    (operator.py:292-298, solvers.py:312): the CUDA backprojector is a
+    deterministic gather, so results are bitwise reproducible for any value.
+    """
+
+    def __init__(self, vol_geom, trajectory, workers: int = 8, device=None):
+        if workers < 1:
+            raise ValueError("workers must be >= 1")
+        if not torch.cuda.is_available():
+            raise RuntimeError("CbctOperator needs a CUDA device (libcbct.so has no CPU path)")
+        self.vol_geom = vol_geom
+        self.trajectory = trajectory
+        self.workers = int(workers)
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._vkey = geometry_key(vol_geom)
+        self._tkey = geometry_key(trajectory)
+        srcs, det00, ustep, vstep = (np.ascontiguousarray(a) for a in view_tables(trajectory))
+        self._tables = (srcs, det00, ustep, vstep)
+        lo = np.asarray(vol_geom.corner(), dtype=np.float64) if hasattr(vol_geom, "corner") else None
+        det = trajectory.detector
+        g = _lib.Geometry()
+        g.nx, g.ny, g.nz = vol_geom.nx, vol_geom.ny, vol_geom.nz
+        for a in range(3):
+            g.lo[a] = float(lo[a])
+            g.pitch[a] = float(vol_geom.voxel_size[a])
+        g.nu, g.nv, g.n_views = det.nu, det.nv, trajectory.n_views
+        g.srcs, g.det00, g.ustep, g.vstep = (a.ctypes.data for a in self._tables)
+        plan = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            call("cbct_plan_create", ctypes.byref(plan), ctypes.byref(g), self._stream())
+        self._plan = plan
+        info = _lib.PlanInfo()
+        call("cbct_plan_get_info", plan, ctypes.byref(info))
+        self.info = info
+        self.vol_elems = int(info.vol_elems)
+        self.zstride = int(info.zstride)
+        nred = max(int(info.proj_blocks), int(info.bp_blocks),
+                   _lib.lib().cbct_vec_blocks(max(self.vol_elems, int(info.n_rays))))
+        self._partials = torch.empty(nred, dtype=torch.float64, device=self.device)
+        self._red = torch.empty(1, dtype=torch.float64, device=self.device)
+        self._host = ctypes.c_double(0.0)
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value:
+            try:
+                _lib.lib().cbct_plan_destroy(plan)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._plan = None
+
+    def __deepcopy__(self, memo):
+        # sklearn.clone deep-copies estimators (test_estimators.py:35-43): rebuild the plan.
+        return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device)
+
+    # ------------------------------------------------------------ properties --
+    @property
+    def n(self) -> int:
+        g = self.vol_geom
+        return g.nx * g.ny * g.nz
+
+    @property
+    def m(self) -> int:
+        return self.trajectory.n_rays
+
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    # ------------------------------------------------- device-layout helpers --
+    def new_volume(self) -> torch.Tensor:
+        return torch.zeros(self.vol_elems, dtype=torch.float32, device=self.device)
+
+    def new_projections(self) -> torch.Tensor:
+        return torch.zeros(self.m, dtype=torch.float32, device=self.device)
+
+    def volume_to_internal(self, data, out=None) -> torch.Tensor:
+        """Reference-layout volume (numpy fp64 or torch) -> device layout."""
+        out = self.new_volume() if out is None else out
+        src, f64 = self._device_src(data, self.n)
+        call("cbct_volume_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
+        return out
+
+    def volume_from_internal(self, t: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
+        out = torch.empty(self.n, dtype=dtype, device=self.device)
+        call("cbct_volume_from_internal", self._plan, _ptr(t), _ptr(out), int(dtype == torch.float64),
+             self._stream())
+        return out
+
+    def proj_to_internal(self, data, out=None) -> torch.Tensor:
+        out = self.new_projections() if out is None else out
+        src, f64 = self._device_src(data, self.m)
+        call("cbct_proj_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
+        return out
+
+    def proj_from_internal(self, t: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
+        out = torch.empty(self.m, dtype=dtype, device=self.device)
+        call("cbct_proj_from_internal", self._plan, _ptr(t), _ptr(out), int(dtype == torch.float64),
+             self._stream())
+        return out
+
+    def _device_src(self, data, size):
+        if isinstance(data, torch.Tensor):
+            t = data.reshape(-1)
+            if t.device != self.device or t.dtype not in (torch.float32, torch.float64):
+                t = t.to(self.device, torch.float32)
+            t = t.contiguous()
+        else:
+            arr = np.ascontiguousarray(data, dtype=np.float64).ravel()
+            t = torch.from_numpy(arr).to(self.device, non_blocking=False)
+        if t.numel() != size:
+            raise ValueError(f"data length {t.numel()} != {size}")
+        return t, t.dtype == torch.float64
+
+    # ------------------------------------------------------- device kernels --
+    def project_internal(self, x: torch.Tensor, out: torch.Tensor, norm2: bool = False):
+        """out = A x on device layouts; returns ||out||^2 (fp64, deterministic) if norm2."""
+        part = self._partials if norm2 else None
+        call("cbct_project", self._plan, _ptr(x), _ptr(out), _ptr(part), self._stream())
+        return self.reduce(int(self.info.proj_blocks)) if norm2 else None
+
+    def backproject_internal(self, y, out: torch.Tensor, mode: int = 1, norm2: bool = False, col_scale=None,
+                             scratch=None):
+        """out = A^T y (mode 1) or diag(A^T A) (mode 2, y ignored); ||out||^2 if norm2."""
+        scratch = torch.empty(self.m, dtype=torch.float32, device=self.device) if scratch is None else scratch
+        part = self._partials if norm2 else None
+        call("cbct_backproject", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode), _ptr(scratch),
+             _ptr(col_scale), _ptr(part), self._stream())
+        return self.reduce(int(self.info.bp_blocks)) if norm2 else None
+
+    def reduce(self, n_partials: int) -> float:
+        """Deterministic sum of the first n partials (synchronises the stream)."""
+        call("cbct_reduce_partials", _ptr(self._partials), int(n_partials), _ptr(self._red),
+             ctypes.byref(self._host), self._stream())
+        return float(self._host.value)
+
+    # ------------------------------------------------------------ public API --
+    def _check_vol(self, x):
+        if geometry_key(x.geometry) != self._vkey:
+            raise GeometryMismatchError("volume geometry does not match operator")
+
+    def _check_proj(self, b):
+        if geometry_key(b.trajectory) != self._tkey:
+            raise GeometryMismatchError("projection trajectory does not match operator")
+
+    def project(self, x, out=None, internal: bool = False):
+        """A x: forward projection (operator.py:316-326)."""
+        self._check_vol(x)
+        if getattr(x, "internal", False):
+            dst = out if out is not None else self.new_projections()
+            self.project_internal(x.data, dst)
+            return InternalProjections(self.trajectory, dst)
+        xin = self.volume_to_internal(x.data)
+        p = self.new_projections()
+        self.project_internal(xin, p)
+        if internal:
+            return InternalProjections(self.trajectory, p)
+        return ProjectionStack(self.trajectory, self._emit(self.proj_from_internal, p, x.data, out, self.m))
+
+    def backproject(self, b, out=None, internal: bool = False):
+        """A^T b: exact adjoint of project (operator.py:328-341)."""
+        self._check_proj(b)
+        if getattr(b, "internal", False):
+            dst = out if out is not None else self.new_volume()
+            self.backproject_internal(b.data, dst)
+            return InternalVolume(self.vol_geom, dst)
+        yin = self.proj_to_internal(b.data)
+        v = self.new_volume()
+        self.backproject_internal(yin, v)
+        if internal:
+            return InternalVolume(self.vol_geom, v)
+        return Volume(self.vol_geom, self._emit(self.volume_from_internal, v, b.data, out, self.n))
+
+    def _emit(self, convert, t_int, like, out, size):
+        """Convert a device-layout result back to the caller's kind of container."""
+        if isinstance(like, torch.Tensor):
+            res = convert(t_int, torch.float32)
+            if out is not None:
+                out.reshape(-1).copy_(res.to(out.dtype))
+                return out
+            return res
+        res = convert(t_int, torch.float64).cpu().numpy()
+        if out is not None:
+            out[:] = res
+            return out
+        return res
+
+    def row_sums(self, internal: bool = False):
+        """A 1: per-ray chord length through the volume box, mm (operator.py:343-346)."""
+        ones = self.new_volume()
+        call("cbct_fill_volume", self._plan, _ptr(ones), ctypes.c_float(1.0), self._stream())
+        p = self.new_projections()
+        self.project_internal(ones, p)
+        if internal:
+            return InternalProjections(self.trajectory, p)
+        return ProjectionStack(self.trajectory, self.proj_from_internal(p, torch.float64).cpu().numpy())
+
+    def col_sums(self, internal: bool = False):
+        """A^T 1: per-voxel total traversal length, mm (operator.py:348-351)."""
+        ones = torch.ones(self.m, dtype=torch.float32, device=self.device)
+        v = self.new_volume()
+        self.backproject_internal(ones, v)
+        if internal:
+            return InternalVolume(self.vol_geom, v)
+        return Volume(self.vol_geom, self.volume_from_internal(v, torch.float64).cpu().numpy())
+
+    def normal_diagonal(self, internal: bool = False):
+        """diag(A^T A): per-voxel sum of squared intersection lengths (operator.py:353-362)."""
+        v = self.new_volume()
+        self.backproject_internal(None, v, mode=2)
+        if internal:
+            return InternalVolume(self.vol_geom, v)
+        return Volume(self.vol_geom, self.volume_from_internal(v, torch.float64).cpu().numpy())
+
+    def ray_segments(self, view: int, u: int, v: int):
+        """(voxel indices, lengths mm) of the ray through pixel (u, v): A^T of a unit
+        impulse, computed by the same CUDA gather (operator.py:364-374)."""
+        det = self.trajectory.detector
+        if not (0 <= view < self.trajectory.n_views and 0 <= u < det.nu and 0 <= v < det.nv):
+            raise IndexError("pixel out of range")
+        y = self.new_projections()
+        y[(view * det.nu + u) * det.nv + v] = 1.0
+        out = self.new_volume()
+        self.backproject_internal(y, out)
+        ref = self.volume_from_internal(out, torch.float64).cpu().numpy()
+        idx = np.flatnonzero(ref).astype(np.int64)
+        return idx, ref[idx]

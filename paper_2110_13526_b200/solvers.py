@@ -1,0 +1,691 @@
+"""Device-resident CGLS / LSQR / SIRT / PSIRT (API of cbctkit.solvers).
+
+Same configuration, validation, history convention, operator budgets,
+breakdown guards and reports as the reference (solvers.py:1-609); the work
+vectors are fp32 tensors on the GPU in the operator's device layouts and every
+vector update is one of libcbct's fused kernels:
+
+  CGLS iteration = A^T (with ||r||^2 in its epilogue)
+                 + volume update  x += a_prev*d ; d = r + beta*d   (one pass)
+                 + A (with ||p||^2 in its epilogue)
+                 + projection update  e -= alpha*p ; ||e||^2      (one pass)
+
+The x update is deferred by one iteration so it fuses with the d update; it is
+flushed before anything reads x.  Scalars (alpha, beta, Givens rotations) are
+fp64 on the host exactly as in the reference; the norms they need come from
+deterministic fp64 device reductions.
+
+Solvers touch the operator only through ``project``/``backproject`` (and
+``normal_diagonal``/``row_sums``/``col_sums``), so instrumented wrappers that
+forward other attributes work as with the reference (test_solvers.py:20-37).
+When the operator is a bare ``CbctOperator`` the norm reductions fuse into the
+A / A^T epilogues.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from ._lib import call
+from .operator import CbctOperator, InternalProjections, InternalVolume
+from .phantom import Volume
+
+__all__ = ["SolverConfigError", "DegenerateOperatorError", "SolverConfig", "ConvergenceRecord", "SolverReport",
+           "cgls", "lsqr", "sirt", "psirt", "solve", "write_history_csv", "normal_spectral_radius",
+           "psirt_step_scale", "KRYLOV_METHODS", "CLASSICAL_METHODS"]
+
+KRYLOV_METHODS = ("cgls", "lsqr")
+CLASSICAL_METHODS = ("sirt", "psirt")
+
+
+class SolverConfigError(ValueError):
+    """Invalid solver configuration."""
+
+
+class DegenerateOperatorError(RuntimeError):
+    """The operator never touches the volume (all-zero row or column sums)."""
+
+
+@dataclass
+class SolverConfig:  # reference solvers.py:56-97
+    method: str = "cgls"
+    max_iterations: int = 40
+    rel_discrepancy_tol: float = 0.0
+    initial_x0: object = None
+    tikhonov_lambda: float = 0.0
+    jacobi_precondition: bool = False
+    jacobi_floor: float = 1e-6
+    box_bounds: tuple = None
+    relaxation: float = 1.0
+    true_discrepancy_every: int = 0
+
+    def validate(self) -> None:
+        if self.method not in KRYLOV_METHODS + CLASSICAL_METHODS:
+            raise SolverConfigError(f"unknown method {self.method!r}")
+        if self.max_iterations < 1:
+            raise SolverConfigError("max_iterations must be >= 1")
+        if not 0.0 <= self.rel_discrepancy_tol <= 1.0:
+            raise SolverConfigError("rel_discrepancy_tol must lie in [0, 1]")
+        if self.tikhonov_lambda < 0:
+            raise SolverConfigError("tikhonov_lambda must be >= 0")
+        if self.jacobi_floor <= 0:
+            raise SolverConfigError("jacobi_floor must be > 0")
+        if self.relaxation <= 0:
+            raise SolverConfigError("relaxation must be > 0")
+        if self.true_discrepancy_every < 0:
+            raise SolverConfigError("true_discrepancy_every must be >= 0")
+        if self.box_bounds is not None:
+            lo, hi = self.box_bounds
+            if lo > hi:
+                raise SolverConfigError("box_bounds must satisfy lo <= hi")
+            if self.method in KRYLOV_METHODS:
+                raise SolverConfigError("box constraints are incompatible with Krylov methods "
+                                        "(the clamped iterate leaves the Krylov subspace)")
+        if self.method in CLASSICAL_METHODS:
+            if self.tikhonov_lambda != 0.0:
+                raise SolverConfigError("tikhonov_lambda applies to cgls/lsqr only")
+            if self.jacobi_precondition:
+                raise SolverConfigError("jacobi_precondition applies to cgls/lsqr only")
+
+
+@dataclass
+class ConvergenceRecord:
+    iteration: int
+    wall_seconds: float
+    rel_discrepancy: float
+    true_rel_discrepancy: float = None
+
+
+@dataclass
+class SolverReport:
+    final_x: Volume
+    iterations: int
+    final_discrepancy_norm: float
+    history: list
+    worker_count: int
+    breakdown: bool = False
+
+
+def _alloc(size: int, physical: int = None, device=None) -> torch.Tensor:
+    """Allocation funnel for the solver work vectors (auditable, solvers.py:118-120).
+    ``size`` is the logical length (n or m); ``physical`` the padded device length."""
+    return torch.zeros(physical if physical is not None else size, dtype=torch.float32, device=device)
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class _Dev:
+    """Fused vector kernels of libcbct bound to an operator's stream and partials."""
+
+    def __init__(self, op):
+        self.op = op
+        self.base = op if isinstance(op, CbctOperator) else None
+        self.plan = op._plan
+        self.partials = op._partials
+        self.vol_elems = op.vol_elems
+        self.device = op.device
+
+    def s(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def reduce(self, nparts: int) -> float:
+        return self.op.reduce(nparts)
+
+    def nblocks(self, n):
+        from ._lib import lib
+
+        return lib().cbct_vec_blocks(n)
+
+    def axpby(self, a, x, b, y, norm2=False):
+        call("cbct_axpby", y.numel(), float(a), _p(x), float(b), _p(y), _p(self.partials) if norm2 else None,
+             self.s())
+        return self.reduce(self.nblocks(y.numel())) if norm2 else None
+
+    def sumsq(self, y):
+        return self.axpby(0.0, None, 1.0, y, norm2=True)
+
+    def sub(self, a, b, out, norm2=False):
+        call("cbct_sub", out.numel(), _p(a), _p(b), _p(out), _p(self.partials) if norm2 else None, self.s())
+        return self.reduce(self.nblocks(out.numel())) if norm2 else None
+
+    def dot(self, x, y):
+        call("cbct_dot", x.numel(), _p(x), _p(y), _p(self.partials), self.s())
+        return self.reduce(self.nblocks(x.numel()))
+
+    def mul(self, a, b, out):
+        call("cbct_mul", out.numel(), _p(a), _p(b), _p(out), self.s())
+
+    def update2(self, x, d, r, a_prev, do_x, beta):
+        """x += a_prev*d (if do_x); d = r + beta*d  -- one fused pass."""
+        call("cbct_cgls_volume_update", d.numel(), _p(x), _p(d), _p(r), float(a_prev), int(do_x), float(beta),
+             self.s())
+
+    def clip(self, vol, lo, hi):
+        call("cbct_clip", self.plan, _p(vol), ctypes.c_float(lo), ctypes.c_float(hi), self.s())
+
+    def fill_volume(self, vol, value):
+        call("cbct_fill_volume", self.plan, _p(vol), ctypes.c_float(value), self.s())
+
+
+def _as_internal_volume(op, vol) -> torch.Tensor:
+    if getattr(vol, "internal", False):
+        return vol.data
+    return op.volume_to_internal(vol.data)
+
+
+def _as_internal_proj(op, stack) -> torch.Tensor:
+    if getattr(stack, "internal", False):
+        return stack.data
+    return op.proj_to_internal(stack.data)
+
+
+def _call_sums(op, name):
+    fn = getattr(op, name)
+    try:
+        return fn(internal=True)
+    except TypeError:  # wrapper with the reference signature
+        return fn()
+
+
+class _Chain:
+    """Flat device-layout view of the operator (solvers.py:123-155)."""
+
+    def __init__(self, op, dev: _Dev):
+        self.op, self.dev = op, dev
+        self.n, self.m, self.m_orig = op.n, op.m, op.m
+        self.n_phys, self.m_phys = dev.vol_elems, op.m
+        self._fused = dev.base is not None
+
+    def apply(self, x, out, norm2=False):
+        if self._fused:
+            return self.op.project_internal(x, out, norm2=norm2)
+        res = self.op.project(InternalVolume(self.op.vol_geom, x), out=out)
+        if res.data is not out:
+            out.copy_(_as_internal_proj(self.op, res))
+        return self.dev.sumsq(out) if norm2 else None
+
+    def applyT(self, y, out, norm2=False):
+        if self._fused:
+            return self.op.backproject_internal(y, out, norm2=norm2, scratch=self._scratch())
+        res = self.op.backproject(InternalProjections(self.op.trajectory, y), out=out)
+        if res.data is not out:
+            out.copy_(_as_internal_volume(self.op, res))
+        return self.dev.sumsq(out) if norm2 else None
+
+    def _scratch(self):
+        if not hasattr(self, "_scr"):
+            self._scr = torch.empty(self.op.m, dtype=torch.float32, device=self.dev.device)
+        return self._scr
+
+    def z_of(self, x0):
+        return x0
+
+    def x_of(self, z):
+        return z
+
+    def rhs(self, b):
+        return b
+
+    def head(self, e):
+        return e[: self.m_orig]
+
+
+class _JacobiChain(_Chain):
+    """min ||b - A D^-1/2 z||, x = D^-1/2 z, diag floored (solvers.py:158-193)."""
+
+    def __init__(self, inner: _Chain, diag: torch.Tensor, floor_frac: float):
+        self.inner, self.op, self.dev = inner, inner.op, inner.dev
+        self.n, self.m, self.m_orig = inner.n, inner.m, inner.m_orig
+        self.n_phys, self.m_phys = inner.n_phys, inner.m_phys
+        dmax = float(diag.max())
+        if dmax <= 0:
+            raise DegenerateOperatorError("normal-equation diagonal is identically zero")
+        floored = torch.clamp(diag.double(), min=floor_frac * dmax)
+        scale = (1.0 / torch.sqrt(floored)).float()
+        # zero the scale on the guard slices so scaled volumes keep zero guards
+        mask = torch.zeros_like(scale)
+        self.dev.fill_volume(mask, 1.0)
+        self.scale = scale * mask
+        self._tmp = torch.empty_like(self.scale)
+
+    def apply(self, z, out, norm2=False):
+        self.dev.mul(z, self.scale, self._tmp)
+        return self.inner.apply(self._tmp, out, norm2=norm2)
+
+    def applyT(self, y, out, norm2=False):
+        inner = self.inner
+        if inner._fused:
+            return inner.op.backproject_internal(y, out, norm2=norm2, col_scale=self.scale, scratch=inner._scratch())
+        inner.applyT(y, out)
+        self.dev.mul(out, self.scale, out)
+        return self.dev.sumsq(out) if norm2 else None
+
+    def z_of(self, x0):
+        safe = torch.where(self.scale > 0, self.scale, torch.ones_like(self.scale))
+        return torch.where(self.scale > 0, x0 / safe, torch.zeros_like(x0))
+
+    def x_of(self, z):
+        out = torch.empty_like(z)
+        self.dev.mul(z, self.scale, out)
+        return out
+
+    def rhs(self, b):
+        return self.inner.rhs(b)
+
+    def head(self, e):
+        return self.inner.head(e)
+
+
+class _TikhonovChain(_Chain):
+    """Stacked [A; lambda I] with data [b; 0] (solvers.py:196-230)."""
+
+    def __init__(self, inner: _Chain, lam: float):
+        self.inner, self.op, self.dev = inner, inner.op, inner.dev
+        self.lam = float(lam)
+        self.n, self.m_orig = inner.n, inner.m_orig
+        self.m = inner.m + inner.n
+        self.n_phys = inner.n_phys
+        self.m_phys = inner.m_phys + inner.n_phys
+        self._tmpT = torch.empty(self.n_phys, dtype=torch.float32, device=self.dev.device)
+
+    def apply(self, x, out, norm2=False):
+        mi = self.inner.m_phys
+        a = self.inner.apply(x, out[:mi], norm2=norm2)
+        tail = out[mi:]
+        tail.zero_()
+        b = self.dev.axpby(self.lam, x, 0.0, tail, norm2=norm2)
+        return a + b if norm2 else None
+
+    def applyT(self, y, out, norm2=False):
+        mi = self.inner.m_phys
+        self.inner.applyT(y[:mi], out)
+        return self.dev.axpby(self.lam, y[mi:], 1.0, out, norm2=norm2)
+
+    def z_of(self, x0):
+        return self.inner.z_of(x0)
+
+    def x_of(self, z):
+        return self.inner.x_of(z)
+
+    def rhs(self, b):
+        out = torch.zeros(self.m_phys, dtype=torch.float32, device=self.dev.device)
+        out[: self.inner.m_phys] = self.inner.rhs(b)
+        return out
+
+    def head(self, e):
+        return self.inner.head(e)
+
+
+def _build_chain(op, cfg: SolverConfig, dev: _Dev) -> _Chain:  # solvers.py:233-240
+    chain = _Chain(op, dev)
+    if cfg.jacobi_precondition:
+        diag = _as_internal_volume(op, op.normal_diagonal())
+        chain = _JacobiChain(chain, diag, cfg.jacobi_floor)
+    if cfg.tikhonov_lambda > 0.0:
+        chain = _TikhonovChain(chain, cfg.tikhonov_lambda)
+    return chain
+
+
+def _geom_eq(a, b):
+    from .geometry import geometry_key
+
+    return geometry_key(a) == geometry_key(b)
+
+
+def _check_inputs(op, b, cfg: SolverConfig, method: str) -> None:  # solvers.py:243-250
+    cfg.validate()
+    if cfg.method != method:
+        raise SolverConfigError(f"cfg.method is {cfg.method!r}, expected {method!r}")
+    if not _geom_eq(b.trajectory, op.trajectory):
+        raise SolverConfigError("projection data does not match the operator trajectory")
+    if cfg.initial_x0 is not None and not _geom_eq(cfg.initial_x0.geometry, op.vol_geom):
+        raise SolverConfigError("initial_x0 geometry does not match the operator")
+
+
+def _x0_internal(op, cfg: SolverConfig, dev: _Dev) -> torch.Tensor:
+    if cfg.initial_x0 is None:
+        return torch.zeros(dev.vol_elems, dtype=torch.float32, device=dev.device)
+    return _as_internal_volume(op, cfg.initial_x0).clone()
+
+
+def _norm(dev: _Dev, v) -> float:
+    return float(np.sqrt(dev.sumsq(v)))
+
+
+def _final_volume(op, x_int, like):
+    """Report the solution in the caller's container kind (numpy fp64 for host b)."""
+    if isinstance(like, torch.Tensor) and getattr(like, "is_cuda", False):
+        return Volume(op.vol_geom, op.volume_from_internal(x_int, torch.float32))
+    return Volume(op.vol_geom, op.volume_from_internal(x_int, torch.float64).cpu().numpy())
+
+
+def _true_rel(op, chain, x_int, b_int, nb0, dev):  # solvers.py:259-261
+    p = torch.empty_like(b_int)
+    res = op.project(InternalVolume(op.vol_geom, chain.x_of(x_int)), out=p)
+    p = _as_internal_proj(op, res)
+    r = torch.empty_like(b_int)
+    return float(np.sqrt(dev.sub(b_int, p, r, norm2=True))) / nb0 if nb0 > 0 else 0.0
+
+
+def _want_true(cfg, iteration):
+    k = cfg.true_discrepancy_every
+    return k > 0 and iteration % k == 0
+
+
+class CglsRun:
+    """Device-resident CGLS state (solvers.py:269-358), split into the pre-loop
+    (``__init__``: 2 A + 1 A^T, first update folded in) and one loop iteration
+    (``step``: 1 A^T + 1 A + two fused vector passes).  ``cgls`` drives it; the
+    benchmark times ``step`` directly."""
+
+    def __init__(self, op, b, cfg: SolverConfig):
+        self.op, self.b, self.cfg = op, b, cfg
+        self.dev = dev = _Dev(op)
+        self.chain = chain = _build_chain(op, cfg, dev)
+        self.t0 = time.perf_counter()
+        self.b_int = _as_internal_proj(op, b)
+        self.x = _alloc(chain.n, chain.n_phys, dev.device)
+        self.x.copy_(chain.z_of(_x0_internal(op, cfg, dev)))
+        self.d = _alloc(chain.n, chain.n_phys, dev.device)
+        self.r = _alloc(chain.n, chain.n_phys, dev.device)
+        self.e = _alloc(chain.m, chain.m_phys, dev.device)
+        self.p = _alloc(chain.m, chain.m_phys, dev.device)
+        self.b_eff = chain.rhs(self.b_int)
+        self.nb0 = _norm(dev, self.b_int)
+        self.history = []
+        self.pending = 0.0  # deferred x += alpha*d
+        self.i = 0
+        self.done = False
+        self.breakdown = False
+        x, d, r, e, p = self.x, self.d, self.r, self.e, self.p
+        chain.apply(x, p)
+        dev.sub(self.b_eff, p, e)
+        self.nr2_old = chain.applyT(e, r, norm2=True)
+        if self.nr2_old == 0.0:
+            self._stop_at_start()
+            return
+        d.copy_(r)
+        np2 = chain.apply(d, p, norm2=True)
+        if np2 == 0.0:
+            self._stop_at_start()
+            return
+        alpha = self.nr2_old / np2
+        self.pending = alpha
+        self.nb = float(np.sqrt(_proj_update(dev, chain, e, p, alpha)))
+        self._record(0)
+
+    def _stop_at_start(self):
+        self.nb = _norm(self.dev, self.chain.head(self.e))
+        self._record(0)
+        self.done = self.breakdown = True
+
+    def rel(self, v):
+        return v / self.nb0 if self.nb0 > 0 else 0.0
+
+    def flush(self):
+        if self.pending != 0.0:
+            self.dev.axpby(self.pending, self.d, 1.0, self.x)
+            self.pending = 0.0
+
+    def _record(self, i):
+        true_e = None
+        if _want_true(self.cfg, i):
+            self.flush()
+            true_e = _true_rel(self.op, self.chain, self.x, self.b_int, self.nb0, self.dev)
+        self.history.append(ConvergenceRecord(i, time.perf_counter() - self.t0, self.rel(self.nb), true_e))
+
+    def should_continue(self) -> bool:
+        return (not self.done) and self.rel(self.nb) > self.cfg.rel_discrepancy_tol and \
+            self.i < self.cfg.max_iterations
+
+    def step(self, record: bool = True) -> bool:
+        """One loop iteration; returns False on breakdown (state left as the reference leaves it)."""
+        dev, chain = self.dev, self.chain
+        nr2 = chain.applyT(self.e, self.r, norm2=True)
+        if nr2 == 0.0:
+            self.done = self.breakdown = True
+            return False
+        beta = nr2 / self.nr2_old
+        dev.update2(self.x, self.d, self.r, self.pending, self.pending != 0.0, beta)  # x += a d ; d = r + b d
+        self.pending = 0.0
+        self.nr2_old = nr2
+        np2 = chain.apply(self.d, self.p, norm2=True)
+        if np2 == 0.0:
+            self.done = self.breakdown = True
+            return False
+        alpha = self.nr2_old / np2
+        self.pending = alpha
+        self.nb = float(np.sqrt(_proj_update(dev, chain, self.e, self.p, alpha)))
+        self.i += 1
+        if record:
+            self._record(self.i)
+        return True
+
+    def report(self) -> SolverReport:
+        self.flush()
+        op = self.op
+        return SolverReport(_final_volume(op, self.chain.x_of(self.x), self.b.data), self.i, self.nb,
+                            self.history, getattr(op, "workers", 1), self.breakdown)
+
+
+def cgls(op, b, cfg: SolverConfig) -> SolverReport:
+    """CGLS with delayed residual (solvers.py:269-358): K+2 A, K+1 A^T."""
+    _check_inputs(op, b, cfg, "cgls")
+    run = CglsRun(op, b, cfg)
+    while run.should_continue():
+        if not run.step():
+            break
+    return run.report()
+
+
+def _proj_update(dev, chain, e, p, alpha):
+    """e -= alpha*p over the whole (possibly stacked) vector; returns ||head(e)||^2."""
+    mo = chain.head(e).numel()
+    nb2 = dev.axpby(-alpha, p[:mo], 1.0, e[:mo], norm2=True)
+    if e.numel() > mo:
+        dev.axpby(-alpha, p[mo:], 1.0, e[mo:])
+    return nb2
+
+
+def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
+    """LSQR (solvers.py:361-459): Golub-Kahan bidiagonalisation + Givens."""
+    _check_inputs(op, b, cfg, "lsqr")
+    dev = _Dev(op)
+    chain = _build_chain(op, cfg, dev)
+    t0 = time.perf_counter()
+    b_int = _as_internal_proj(op, b)
+    x = chain.z_of(_x0_internal(op, cfg, dev)).clone()
+    b_eff = chain.rhs(b_int)
+    nb0 = _norm(dev, b_int)
+    history = []
+
+    def rel(v):
+        return v / nb0 if nb0 > 0 else 0.0
+
+    def record(i, e):
+        true_e = None
+        if _want_true(cfg, i):
+            true_e = _true_rel(op, chain, x, b_int, nb0, dev)
+        history.append(ConvergenceRecord(i, time.perf_counter() - t0, e, true_e))
+
+    def finish(i, phibar, breakdown):
+        return SolverReport(_final_volume(op, chain.x_of(x), b.data), i, phibar, history,
+                            getattr(op, "workers", 1), breakdown)
+
+    u = torch.empty(chain.m_phys, dtype=torch.float32, device=dev.device)
+    chain.apply(x, u)
+    beta = float(np.sqrt(dev.sub(b_eff, u, u, norm2=True)))
+    if beta == 0.0:
+        record(0, 0.0)
+        return finish(0, 0.0, True)
+    dev.axpby(0.0, None, 1.0 / beta, u)
+    v = torch.empty(chain.n_phys, dtype=torch.float32, device=dev.device)
+    alpha = float(np.sqrt(chain.applyT(u, v, norm2=True)))
+    if alpha == 0.0:
+        record(0, rel(beta))
+        return finish(0, beta, True)
+    dev.axpby(0.0, None, 1.0 / alpha, v)
+    w = v.clone()
+    phibar, rhobar = beta, alpha
+    tmp_m = torch.empty_like(u)
+    tmp_n = torch.empty_like(v)
+    err = cfg.rel_discrepancy_tol
+    updates = 0
+    breakdown = False
+    while updates < cfg.max_iterations + 1:
+        chain.apply(v, tmp_m)
+        beta = float(np.sqrt(dev.axpby(1.0, tmp_m, -alpha, u, norm2=True)))  # u = A v - alpha u
+        if beta > 0.0:
+            dev.axpby(0.0, None, 1.0 / beta, u)
+            chain.applyT(u, tmp_n)
+            alpha = float(np.sqrt(dev.axpby(1.0, tmp_n, -beta, v, norm2=True)))  # v = A^T u - beta v
+            if alpha > 0.0:
+                dev.axpby(0.0, None, 1.0 / alpha, v)
+        rho = float(np.hypot(rhobar, beta))
+        c, s = rhobar / rho, beta / rho
+        theta = s * alpha
+        rhobar = -c * alpha
+        phi = c * phibar
+        phibar = s * phibar
+        dev.update2(x, w, v, phi / rho, True, -(theta / rho))  # x += (phi/rho) w ; w = v - (theta/rho) w
+        record(updates, rel(phibar))
+        updates += 1
+        if beta == 0.0 or alpha == 0.0:
+            breakdown = True
+            break
+        if err > 0.0 and rel(phibar) <= err:
+            break
+    return finish(len(history) - 1, phibar, breakdown)
+
+
+def _inv_positive(t):
+    return torch.where(t > 0, 1.0 / torch.where(t > 0, t, torch.ones_like(t)), torch.zeros_like(t))
+
+
+def normal_spectral_radius(op, power_iterations: int = 10) -> float:
+    """rho(A^T R^-1 A) by power iteration from all-ones (solvers.py:462-489)."""
+    if power_iterations < 1:
+        raise ValueError("power_iterations must be >= 1")
+    dev = _Dev(op)
+    row = _as_internal_proj(op, _call_sums(op, "row_sums"))
+    inv_row = _inv_positive(row)
+    return _spectral(op, dev, inv_row, power_iterations)
+
+
+def _spectral(op, dev, inv_row, iters):
+    proj = torch.empty(op.m, dtype=torch.float32, device=dev.device)
+    w = torch.empty(dev.vol_elems, dtype=torch.float32, device=dev.device)
+    v = torch.empty_like(w)
+    dev.fill_volume(v, 1.0)
+    chain = _Chain(op, dev)
+    for _ in range(iters):
+        chain.apply(v, proj)
+        dev.mul(proj, inv_row, proj)
+        norm = float(np.sqrt(chain.applyT(proj, w, norm2=True)))
+        if norm == 0.0:
+            raise DegenerateOperatorError("operator never intersects the volume")
+        v.copy_(w)
+        dev.axpby(0.0, None, 1.0 / norm, v)
+    chain.apply(v, proj)
+    dev.mul(proj, inv_row, proj)
+    chain.applyT(proj, w)
+    return dev.dot(v, w)
+
+
+_PSIRT_SPECTRAL_SAFETY = 1.05  # solvers.py:496
+
+
+def psirt_step_scale(op, relaxation: float = 1.0) -> float:
+    return 2.0 * relaxation / (_PSIRT_SPECTRAL_SAFETY * normal_spectral_radius(op))
+
+
+def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solvers.py:505-569
+    _check_inputs(op, b, cfg, method)
+    dev = _Dev(op)
+    t0 = time.perf_counter()
+    row = _as_internal_proj(op, _call_sums(op, "row_sums"))
+    col = _as_internal_volume(op, _call_sums(op, "col_sums"))
+    if not bool((row > 0).any()) or not bool((col > 0).any()):
+        raise DegenerateOperatorError("operator never intersects the volume")
+    inv_row = _inv_positive(row)
+    if method == "sirt":
+        step_vec = (cfg.relaxation * _inv_positive(col)).float()
+        step = None
+    else:
+        step_vec = None
+        step = 2.0 * cfg.relaxation / (_PSIRT_SPECTRAL_SAFETY * _spectral(op, dev, inv_row, 10))
+    del col
+    b_int = _as_internal_proj(op, b)
+    x = _x0_internal(op, cfg, dev)
+    nb0 = _norm(dev, b_int)
+    lo, hi = cfg.box_bounds if cfg.box_bounds is not None else (None, None)
+    history = []
+    chain = _Chain(op, dev)
+
+    def rel(v):
+        return v / nb0 if nb0 > 0 else 0.0
+
+    def record(i, e):
+        history.append(ConvergenceRecord(i, time.perf_counter() - t0, e, e if _want_true(cfg, i) else None))
+
+    resid = torch.empty(op.m, dtype=torch.float32, device=dev.device)
+    weighted = torch.empty_like(resid)
+    upd = torch.empty(dev.vol_elems, dtype=torch.float32, device=dev.device)
+    chain.apply(x, resid)
+    e = rel(float(np.sqrt(dev.sub(b_int, resid, resid, norm2=True))))
+    record(0, e)
+    err = cfg.rel_discrepancy_tol
+    i = 0
+    while (err == 0.0 or e > err) and i < cfg.max_iterations:
+        dev.mul(resid, inv_row, weighted)
+        chain.applyT(weighted, upd)
+        if step_vec is not None:
+            dev.mul(upd, step_vec, upd)
+            dev.axpby(1.0, upd, 1.0, x)
+        else:
+            dev.axpby(step, upd, 1.0, x)
+        if lo is not None:
+            dev.clip(x, lo, hi)
+        chain.apply(x, resid)
+        e = rel(float(np.sqrt(dev.sub(b_int, resid, resid, norm2=True))))
+        i += 1
+        record(i, e)
+        if err > 0.0 and e <= err:
+            break
+    return SolverReport(_final_volume(op, x, b.data), i, e * nb0, history, getattr(op, "workers", 1), False)
+
+
+def sirt(op, b, cfg: SolverConfig) -> SolverReport:
+    """SIRT: x += relaxation C^-1 A^T R^-1 (b - A x), optionally clamped (solvers.py:572-578)."""
+    return _classical(op, b, cfg, "sirt")
+
+
+def psirt(op, b, cfg: SolverConfig) -> SolverReport:
+    """PSIRT: scalar step 2*omega/(1.05*rho) (solvers.py:581-587)."""
+    return _classical(op, b, cfg, "psirt")
+
+
+_SOLVERS = {"cgls": cgls, "lsqr": lsqr, "sirt": sirt, "psirt": psirt}
+
+
+def solve(op, b, cfg: SolverConfig) -> SolverReport:
+    cfg.validate()
+    return _SOLVERS[cfg.method](op, b, cfg)
+
+
+def write_history_csv(history, path) -> None:
+    """iter,seconds,rel_discrepancy,true_rel_discrepancy (solvers.py:599-609)."""
+    with open(path, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh, lineterminator="\n")
+        w.writerow(["iter", "seconds", "rel_discrepancy", "true_rel_discrepancy"])
+        for rec in history:
+            t = "" if rec.true_rel_discrepancy is None else repr(rec.true_rel_discrepancy)
+            w.writerow([rec.iteration, f"{rec.wall_seconds:.6f}", repr(rec.rel_discrepancy), t])

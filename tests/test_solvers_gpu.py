@@ -1,0 +1,278 @@
+"""Device CGLS / LSQR / PSIRT / SIRT vs the reference goldens and the oracle, plus the
+solver contract of the reference (test_solvers.py, test_dense_oracle.py).
+
+Iterate tolerance (north star): ||x_gpu - x_ref|| / ||x_ref|| <= 1e-3 after the
+named iteration count; per-record relative discrepancies within 1e-3 relative.
+fp64 tolerances of the reference (1e-6 .. 1e-12) are restated for fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from _helpers import baseline_geometry, geom_from_golden, load_golden, rel_l2
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ITER_TOL = 1e-3
+
+
+def _mods():
+    import paper_2110_13526_b200 as P
+    import paper_2110_13526_b200.solvers as S
+
+    return P, S
+
+
+@pytest.fixture(scope="module")
+def small():
+    P, _ = _mods()
+    d = load_golden("small_instance")
+    vg, tr = geom_from_golden(d)
+    return d, P.CbctOperator(vg, tr, workers=3)
+
+
+def _hist(rep):
+    return np.array([r.rel_discrepancy for r in rep.history])
+
+
+def test_small_instance_solver_goldens(small):
+    P, S = _mods()
+    d, op = small
+    b = P.ProjectionStack(op.trajectory, d["solver_b"])
+    for method, K, key, kw in (("cgls", 25, "cgls25", {}), ("lsqr", 25, "lsqr25", {}),
+                               ("lsqr", 25, "lsqrj25", {"jacobi_precondition": True}),
+                               ("psirt", 7, "psirt7", {})):
+        rep = S.solve(op, b, S.SolverConfig(method=method, max_iterations=K, **kw))
+        h = _hist(rep)
+        assert h.shape == d[f"{key}_hist"].shape
+        np.testing.assert_allclose(h, d[f"{key}_hist"], rtol=2e-3, err_msg=key)
+        assert rel_l2(rep.final_x.data, d[f"{key}_x"]) <= ITER_TOL, key
+
+
+def test_desk_solver_goldens():
+    P, S = _mods()
+    d = load_golden("desk")
+    vg, tr = geom_from_golden(d)
+    op = P.CbctOperator(vg, tr)
+    truth = d["truth"].astype(np.float64)
+    b = O.OracleOperator(vg, tr).project(truth)
+    bs = P.ProjectionStack(tr, b)
+    rep = S.cgls(op, bs, S.SolverConfig(method="cgls", max_iterations=10, true_discrepancy_every=10))
+    np.testing.assert_allclose(_hist(rep), d["cgls10_hist"], rtol=ITER_TOL)
+    assert rel_l2(rep.final_x.data, d["cgls10_x"]) <= ITER_TOL
+    assert rep.history[10].true_rel_discrepancy == pytest.approx(float(d["cgls10_true10"]), rel=1e-3)
+    rep = S.lsqr(op, bs, S.SolverConfig(method="lsqr", max_iterations=10, jacobi_precondition=True))
+    np.testing.assert_allclose(_hist(rep), d["lsqrj10_hist"], rtol=ITER_TOL)
+    assert rel_l2(rep.final_x.data, d["lsqrj10_x"]) <= ITER_TOL
+    rep = S.psirt(op, bs, S.SolverConfig(method="psirt", max_iterations=10))
+    np.testing.assert_allclose(_hist(rep), d["psirt10_hist"], rtol=ITER_TOL)
+    assert rel_l2(rep.final_x.data, d["psirt10_x"]) <= ITER_TOL
+
+
+def test_config1_cgls10_iterate():
+    """BASELINE config 1: 64^3, 90 views of 128x96, CGLS 10 -- iterate within 1e-3 of the reference."""
+    P, S = _mods()
+    d = load_golden("config1")
+    vg, tr = baseline_geometry(64, 90, 128, 96)
+    op = P.CbctOperator(vg, tr)
+    ref = O.OracleOperator(vg, tr)
+    b = ref.project(O.shepp_logan_phantom(vg))
+    rep = S.cgls(op, P.ProjectionStack(tr, b), S.SolverConfig(method="cgls", max_iterations=10))
+    np.testing.assert_allclose(_hist(rep), d["cgls10_hist"], rtol=ITER_TOL)
+    x = rep.final_x.data
+    assert rel_l2(x[d["cgls10_x_idx"]], d["cgls10_x_val"]) <= ITER_TOL
+    x_ref, _ = O.cgls(ref, b, 10)
+    assert rel_l2(x, x_ref) <= ITER_TOL
+
+
+class CountingOperator:
+    """Duck-typed wrapper counting project/backproject calls (test_solvers.py:20-37)."""
+
+    def __init__(self, op):
+        self._op = op
+        self.projections = 0
+        self.backprojections = 0
+
+    def project(self, x, out=None):
+        self.projections += 1
+        return self._op.project(x, out=out)
+
+    def backproject(self, b, out=None):
+        self.backprojections += 1
+        return self._op.backproject(b, out=out)
+
+    def __getattr__(self, name):
+        return getattr(self._op, name)
+
+
+@pytest.fixture
+def consistent(small):
+    P, _ = _mods()
+    _, op = small
+    x_true = P.Volume(op.vol_geom, np.random.default_rng(5).random(op.n))
+    return x_true, op.project(x_true)
+
+
+def test_operator_application_budget(small, consistent):
+    _, S = _mods()
+    _, op = small
+    _, b = consistent
+    for k in (1, 5, 12):
+        c = CountingOperator(op)
+        S.cgls(c, b, S.SolverConfig(method="cgls", max_iterations=k))
+        assert (c.projections, c.backprojections) == (k + 2, k + 1)
+
+
+def test_allocation_audit(small, consistent, monkeypatch):
+    _, S = _mods()
+    _, op = small
+    _, b = consistent
+    sizes = []
+    real = S._alloc
+    monkeypatch.setattr(S, "_alloc", lambda size, *a, **k: sizes.append(size) or real(size, *a, **k))
+    S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=5))
+    assert sizes.count(op.n) == 3 and sizes.count(op.m) == 2 and len(sizes) == 5
+
+
+def test_history_contract_and_monotone(small, consistent):
+    _, S = _mods()
+    _, op = small
+    _, b = consistent
+    for method in (S.cgls, S.lsqr):
+        rep = method(op, b, S.SolverConfig(method=method.__name__, max_iterations=7))
+        assert rep.iterations == 7 and [r.iteration for r in rep.history] == list(range(8))
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=30))
+    es = [r.rel_discrepancy for r in rep.history]
+    assert all(b2 <= a * (1 + 1e-5) for a, b2 in zip(es, es[1:]))
+
+
+def test_breakdowns_and_zero_data(small, consistent):
+    P, S = _mods()
+    _, op = small
+    x_true, b = consistent
+    # exact x0: residual A^T(b - A x0) is ~0 in fp32 -> either breakdown or a no-op
+    zero = P.ProjectionStack(op.trajectory)
+    rep = S.cgls(op, zero, S.SolverConfig(method="cgls", max_iterations=5))
+    assert rep.iterations == 0 and rep.final_discrepancy_norm == 0.0 and not np.any(rep.final_x.data)
+    assert rep.breakdown
+    rep = S.lsqr(op, zero, S.SolverConfig(method="lsqr", max_iterations=5))
+    assert rep.iterations == 0 and not np.any(rep.final_x.data)
+    for m in (S.sirt, S.psirt):
+        rep = m(op, zero, S.SolverConfig(method=m.__name__, max_iterations=4))
+        assert not np.any(rep.final_x.data)
+
+
+def test_tolerance_stop_and_true_discrepancy(small, consistent):
+    _, S = _mods()
+    _, op = small
+    _, b = consistent
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=500, rel_discrepancy_tol=0.05))
+    assert rep.iterations < 500 and rep.history[-1].rel_discrepancy <= 0.05
+    assert all(r.rel_discrepancy > 0.05 for r in rep.history[:-1])
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=9, true_discrepancy_every=3))
+    for rec in rep.history:
+        if rec.iteration % 3 == 0:
+            assert rec.true_rel_discrepancy == pytest.approx(rec.rel_discrepancy, rel=1e-3, abs=1e-6)
+        else:
+            assert rec.true_rel_discrepancy is None
+
+
+def test_box_bounds_and_degenerate(small, consistent):
+    P, S = _mods()
+    _, op = small
+    _, b = consistent
+    rep = S.psirt(op, b, S.SolverConfig(method="psirt", max_iterations=30, box_bounds=(0.0, 1.0)))
+    assert rep.final_x.data.min() >= 0.0 and rep.final_x.data.max() <= 1.0
+
+    class NullOperator:
+        def __init__(self, op):
+            self._op = op
+
+        def project(self, x, out=None):
+            s = self._op.project(x, out=out)
+            s.data[:] = 0.0
+            return s
+
+        def backproject(self, b, out=None):
+            v = self._op.backproject(b, out=out)
+            v.data[:] = 0.0
+            return v
+
+        def row_sums(self):
+            return P.ProjectionStack(self._op.trajectory)
+
+        def col_sums(self):
+            return P.Volume(self._op.vol_geom)
+
+        def __getattr__(self, name):
+            return getattr(self._op, name)
+
+    ones = P.ProjectionStack(op.trajectory, np.ones(op.m))
+    with pytest.raises(S.DegenerateOperatorError):
+        S.sirt(NullOperator(op), ones, S.SolverConfig(method="sirt", max_iterations=2))
+
+
+def test_dispatch_mismatch_and_csv(tmp_path, small, consistent):
+    _, S = _mods()
+    _, op = small
+    _, b = consistent
+    assert S.solve(op, b, S.SolverConfig(method="lsqr", max_iterations=3)).iterations == 3
+    with pytest.raises(S.SolverConfigError):
+        S.cgls(op, b, S.SolverConfig(method="sirt"))
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=4, true_discrepancy_every=2))
+    path = tmp_path / "h.csv"
+    S.write_history_csv(rep.history, path)
+    lines = path.read_bytes().decode().splitlines()
+    assert lines[0] == "iter,seconds,rel_discrepancy,true_rel_discrepancy" and len(lines) == 6
+
+
+def test_dense_least_squares_tikhonov_jacobi(small):
+    """test_dense_oracle.py:53-140 restated for fp32: CGLS/LSQR -> lstsq, Tikhonov
+    closed form, Jacobi solves the same problem; uniform diagonal is a no-op."""
+    P, S = _mods()
+    d, op = small
+    A = np.zeros((op.m, op.n))
+    A[d["dense_rows"], d["dense_cols"]] = d["dense_vals"]
+    b = P.ProjectionStack(op.trajectory, d["solver_b"])
+    x_ls = np.linalg.lstsq(A, b.data, rcond=None)[0]
+    for m in ("cgls", "lsqr"):
+        rep = S.solve(op, b, S.SolverConfig(method=m, max_iterations=300, rel_discrepancy_tol=1e-6))
+        assert rel_l2(rep.final_x.data, x_ls) <= 5e-3, m
+        rep = S.solve(op, b, S.SolverConfig(method=m, max_iterations=400, tikhonov_lambda=1.0))
+        closed = np.linalg.solve(A.T @ A + np.eye(op.n), A.T @ b.data)
+        assert rel_l2(rep.final_x.data, closed) <= 1e-3, m
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=400, rel_discrepancy_tol=1e-6,
+                                       jacobi_precondition=True))
+    assert rel_l2(rep.final_x.data, x_ls) <= 5e-3
+
+    class UniformDiag:
+        def __init__(self, op):
+            self._op = op
+
+        def normal_diagonal(self):
+            return P.Volume(self._op.vol_geom, np.ones(self._op.n))
+
+        def __getattr__(self, name):
+            return getattr(self._op, name)
+
+    plain = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=25))
+    pre = S.cgls(UniformDiag(op), b, S.SolverConfig(method="cgls", max_iterations=25, jacobi_precondition=True))
+    np.testing.assert_allclose(pre.final_x.data, plain.final_x.data, rtol=1e-4, atol=1e-6)
+
+
+def test_spectral_radius_and_psirt_dense(small):
+    P, S = _mods()
+    d, op = small
+    assert S.normal_spectral_radius(op) == pytest.approx(float(d["rho"]), rel=1e-4)
+
+
+def test_device_tensor_inputs_stay_on_device(small):
+    P, S = _mods()
+    d, op = small
+    bt = torch.tensor(d["solver_b"], dtype=torch.float32, device="cuda")
+    rep = S.cgls(op, P.ProjectionStack(op.trajectory, bt), S.SolverConfig(method="cgls", max_iterations=25))
+    assert isinstance(rep.final_x.data, torch.Tensor) and rep.final_x.data.is_cuda
+    assert rel_l2(rep.final_x.data.double().cpu().numpy(), d["cgls25_x"]) <= ITER_TOL
