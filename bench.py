@@ -1,0 +1,354 @@
+"""Benchmark: CGLS iterations/s and GUPS of A / A^T on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 2 -- 3-D Shepp-Logan 256^3, 360 views of a
+512x384 detector, CGLS (SURVEY.md 8(d) geometry rule: SID 749, SDD 1198, 0.86 mm
+voxels, 0.741 mm pixels).  A "step" is one steady-state CGLS loop iteration
+(solvers.py:339-357): A^T (+||r||^2), fused volume update, A (+||p||^2), fused
+projection update (+||e||^2).  Inputs stay resident in HBM; the working set
+(67 MB volume + 3 x 283 MB projection vectors) exceeds the 126 MB L2, so no
+explicit flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
+algorithm's CPU restatement (oracle/, C + OpenMP, all host threads) on a bounded
+view sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# BASELINE.json configs: (N, views, nu, nv, solver, K)
+CONFIGS = {
+    1: (64, 90, 128, 96, "cgls", 10),
+    2: (256, 360, 512, 384, "cgls", 40),
+    3: (512, 720, 616, 480, "cgls", 40),
+    4: (512, 720, 616, 480, "lsqr-jacobi", 40),
+    5: (1024, 1440, 1024, 768, "cgls", 10),
+}
+# nnz(A) per config, SURVEY.md 8(d) (exact for 1-2, sampled for 3-5); the
+# algorithmic unit of the A / A^T roofline.
+NNZ = {1: 8.50e7, 2: 2.176e10, 3: 1.312e11, 4: 1.312e11, 5: 1.36e12}
+SLOTS_PER_NNZ = 8  # FP32-lane-slot equivalents per nonzero
+SMS = 148
+LANES = 128
+
+
+def geometry(cfg: int):
+    from paper_2110_13526_b200.geometry import DetectorGeometry, VolumeGeometry, make_circular_trajectory
+
+    N, V, nu, nv, _, _ = CONFIGS[cfg]
+    p = 220.16 / N
+    vg = VolumeGeometry(N, N, N, (p, p, p))
+    pu = 379.456 / nu
+    tr = make_circular_trajectory(749.0, 1198.0, V, 0.0, 2 * np.pi, DetectorGeometry(nu, nv, (pu, pu)))
+    return vg, tr
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+        return False
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU legs --
+def cpu_sample(cfg: int, nviews: int = None, threads: int = 0):
+    """Reference algorithm (oracle port, C+OpenMP, fp64) on a contiguous view sample of
+    the workload: returns seconds for one A and one A^T scaled to all views, plus the
+    vector-update time, i.e. the CPU time of one CGLS iteration."""
+    from oracle import oracle as O
+    from paper_2110_13526_b200.geometry import make_circular_trajectory
+
+    vg, tr = geometry(cfg)
+    V = tr.n_views
+    threads_avail = int(O.lib().oracle_max_threads()) if threads < 1 else threads
+    # enough views that the worker-parallel backprojector uses every host thread
+    k = nviews or max(1, min(V, max(threads_avail, {1: 90, 2: 6, 3: 2, 4: 2, 5: 1}[cfg])))
+    sub = make_circular_trajectory(tr.sid, tr.sdd, k, 0.0, k * tr.angular_span / V, tr.detector)
+    # backprojector workers as the reference deals them (operator.py:219-220), capped so the
+    # private accumulators stay small
+    workers = max(1, min(threads_avail, k, 64))
+    op = O.OracleOperator(vg, sub, workers=workers, threads=threads)
+    x = np.random.default_rng(0).random(op.n)
+    y = np.random.default_rng(1).standard_normal(op.m)
+    t0 = time.perf_counter()
+    op.project(x)
+    ta = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    op.backproject(y)
+    tat = time.perf_counter() - t0
+    scale = V / k
+    # vector work of one CGLS iteration in fp64 numpy (solvers.py:340-355), full size
+    n, m = vg.nx * vg.ny * vg.nz, tr.n_rays
+    xv, dv, rv = np.zeros(n), np.ones(n), np.ones(n)
+    t0 = time.perf_counter()
+    _ = float(rv @ rv)
+    dv *= 0.5
+    dv += rv
+    xv += 0.1 * dv
+    tv_n = time.perf_counter() - t0
+    del xv, dv, rv
+    ev, pv = np.ones(m), np.ones(m)
+    t0 = time.perf_counter()
+    _ = float(pv @ pv)
+    ev -= 0.1 * pv
+    _ = float(np.linalg.norm(ev))
+    tv_m = time.perf_counter() - t0
+    del ev, pv
+    t_iter = ta * scale + tat * scale + tv_n + tv_m
+    return {"t_A": ta * scale, "t_AT": tat * scale, "t_vec": tv_n + tv_m, "t_iter": t_iter,
+            "views_sampled": k, "threads": int(O.lib().oracle_max_threads()) if threads < 1 else threads}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    samples = []
+    for _ in range(args.warmup):
+        cpu_sample(cfg)
+    for _ in range(args.steps):
+        samples.append(cpu_sample(cfg))
+    t_iter = float(np.median([s["t_iter"] for s in samples]))
+    N, V, nu, nv, solver, K = CONFIGS[cfg]
+    s0 = samples[0]
+    val = 1.0 / t_iter
+    line = {
+        "impl": "reference", "metric": "CGLS iterations/sec", "value": val, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_iter * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, {solver}",
+                   "parallelism": "cpu-openmp"},
+        "gups_A": N ** 3 * V / s0["t_A"] / 1e9, "gups_AT": N ** 3 * V / s0["t_AT"] / 1e9,
+        "cpu_baseline": {"value": val, "unit": "it/s", "cores": s0["threads"], "kind": "port",
+                         "sample": f"A and A^T on {s0['views_sampled']} of {V} views, scaled by views; "
+                                   f"vector updates at full size (numpy fp64)"},
+        "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg --
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200 import _lib
+    from paper_2110_13526_b200.solvers import CglsRun, SolverConfig
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    N, V, nu, nv, solver, K = CONFIGS[cfg]
+    vg, tr = geometry(cfg)
+    t_setup = time.perf_counter()
+    op = P.CbctOperator(vg, tr, device=dev)
+    truth = P.generate_phantom(P.shepp_logan_3d(), vg)
+    x_t = torch.from_numpy(truth.data).to(dev)
+    b_int = op.project(P.Volume(vg, x_t), internal=True).data  # inverse crime b = A phantom (fp32, device)
+    b = P.operator.InternalProjections(tr, b_int)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+    steps, warmup = args.steps, args.warmup
+    scfg = SolverConfig(method="cgls", max_iterations=steps + warmup + 1)
+    run = CglsRun(op, b, scfg)
+    stream = torch.cuda.current_stream(dev)
+
+    # kernel timers: events bracketing A and A^T inside the timed loop (same stream)
+    chain = run.chain
+    ev = {"A": [], "AT": []}
+    orig_apply, orig_applyT = chain.apply, chain.applyT
+
+    def timed(name, fn):
+        def wrapper(*a, **k):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            out = fn(*a, **k)
+            e.record(stream)
+            ev[name].append((s, e))
+            return out
+        return wrapper
+
+    for _ in range(warmup):
+        run.step(record=False)
+    chain.apply, chain.applyT = timed("A", orig_apply), timed("AT", orig_applyT)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().cbct_launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        start.record(stream)
+        for _ in range(steps):
+            run.step(record=False)
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.lib().cbct_launch_count() - launches0
+    chain.apply, chain.applyT = orig_apply, orig_applyT
+    ms = start.elapsed_time(end)
+    # in-loop A / A^T durations (include the fused norm reduction and its host read)
+    t_a_loop = float(np.mean([s.elapsed_time(e) for s, e in ev["A"]]))
+    t_at_loop = float(np.mean([s.elapsed_time(e) for s, e in ev["AT"]]))
+    # kernel-only durations: CUDA events tight around the launches on this stream
+    scratch = torch.empty(op.m, dtype=torch.float32, device=dev)
+
+    def kernel_ms(fn, reps=5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(reps):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    t_a = kernel_ms(lambda: op.project_internal(run.d, run.p))
+    t_at = kernel_ms(lambda: op.backproject_internal(run.e, run.r, scratch=scratch))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / steps
+    value = world * 1e3 / ms_step  # replicas: every rank runs the whole iteration
+
+    # end-to-end through the public API: host fp64 b in, host x out, full solve
+    b_host = op.proj_from_internal(b_int, torch.float64).cpu().numpy()
+    e2e_k = max(steps, 5)
+    bstack = P.ProjectionStack(tr, b_host)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = P.cgls(op, bstack, SolverConfig(method="cgls", max_iterations=e2e_k))
+    torch.cuda.synchronize()
+    t_e2e = time.perf_counter() - t0
+    e2e = {"value": rep.iterations / t_e2e, "unit": "it/s",
+           "h2d_bytes_per_step": int(op.m * 8 / e2e_k), "d2h_bytes_per_step": int((op.n * 8 + 24 * e2e_k) / e2e_k),
+           "note": f"cgls() on host fp64 ProjectionStack, K={e2e_k}, incl. pre-loop (2 A + 1 A^T) and copies"}
+
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    f_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    peak_slots = SMS * LANES * f_mhz * 1e6
+    nnz = NNZ[cfg]
+    dom, t_dom = ("A^T", t_at) if t_at >= t_a else ("A", t_a)
+    achieved = SLOTS_PER_NNZ * nnz / (t_dom * 1e-3)
+    roof = {"bound": "issue", "kernel": f"{dom} ({'k_backproject' if dom == 'A^T' else 'k_project'})",
+            "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
+            "traffic": None,
+            "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
+                          f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
+            "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
+            "frac_AT": SLOTS_PER_NNZ * nnz / (t_at * 1e-3) / peak_slots}
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        s = cpu_sample(cfg)
+        cpu = {"value": 1.0 / s["t_iter"], "unit": "it/s", "cores": s["threads"], "kind": "port",
+               "sample": f"oracle A+A^T on {s['views_sampled']}/{V} views scaled to all views + full-size numpy "
+                         f"vector updates; t_A {s['t_A']:.2f}s t_AT {s['t_AT']:.2f}s"}
+    line = {
+        "metric": "CGLS iterations/sec", "value": value, "unit": "it/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "working set > 126 MB L2 (no flush needed)"},
+        "gups_A": N ** 3 * V / (t_a * 1e-3) / 1e9, "gups_AT": N ** 3 * V / (t_at * 1e-3) / 1e9,
+        "ms_A": t_a, "ms_AT": t_at, "ms_A_in_loop": t_a_loop, "ms_AT_in_loop": t_at_loop,
+        "ms_vector_and_host": ms_step - t_a_loop - t_at_loop,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
+        "setup_s": t_setup, "plan_table_bytes": int(op.info.table_bytes),
+        "e_last": run.rel(run.nb),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, args.config, rank, world)
+    if world > 1:
+        import torch
+
+        torch.distributed.init_process_group("nccl")
+    rc = run_ours(args, args.config, rank, world, local_rank)
+    if world > 1:
+        import torch
+
+        torch.distributed.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -17,6 +17,7 @@
 // fp32 min/max/fma.
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "cbct_internal.cuh"
 #include "reduce.cuh"
@@ -42,11 +43,12 @@ __global__ void k_weight_rays(const ColumnHeader* __restrict__ cols, const doubl
     yw[i] = y ? len * y[i] : len;
 }
 
-template <int ZPT>
+template <int ZPT, bool PRECISE>
 __global__ void __launch_bounds__(512) k_backproject(const int64_t* __restrict__ cell_off,
                                                      const CellEntry* __restrict__ cell_ent,
                                                      const ColumnHeader* __restrict__ cols,
-                                                     const float* __restrict__ invw, const float* __restrict__ yw,
+                                                     const float* __restrict__ invw, const double* __restrict__ wtab,
+                                                     const float* __restrict__ yw,
                                                      float* __restrict__ vol, const float* __restrict__ col_scale,
                                                      double* __restrict__ partials, int nv, int nz, int zs,
                                                      double lo2, double p2, double det00z, double pv, int flat_v,
@@ -102,6 +104,11 @@ __global__ void __launch_bounds__(512) k_backproject(const int64_t* __restrict__
                     float d;
                     if (v == flat_v) {
                         d = (iz[r] == t.flat_slab) ? t.tb - t.ta : 0.0f;
+                    } else if (PRECISE) {  // fp64 z clip (diagnostic / reference-precision path)
+                        const double w = wtab[v];
+                        const double u1 = (lo2 + (double)iz[r] * p2) / w - (double)t.tref;
+                        const double u2 = (lo2 + (double)(iz[r] + 1) * p2) / w - (double)t.tref;
+                        d = (float)(fmin((double)t.tb, fmax(u1, u2)) - fmax((double)t.ta, fmin(u1, u2)));
                     } else {
                         const float iw = s_invw[v];
                         const float u1 = fmaf(z0[r], iw, -t.tref);
@@ -152,20 +159,25 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
     CBCT_CHECK(cudaGetLastError());
     const size_t smem = (size_t)p->nv * sizeof(float);
     const dim3 grid((unsigned)p->n_cells);
-#define LAUNCH(Z)                                                                                             \
+#define LAUNCH(Z, PR)                                                                                         \
     do {                                                                                                      \
         if (smem > 40 * 1024)                                                                                 \
-            CBCT_CHECK(cudaFuncSetAttribute(k_backproject<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+            CBCT_CHECK(cudaFuncSetAttribute(k_backproject<Z, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                             (int)smem));                                                      \
-        k_backproject<Z><<<grid, p->bp_threads, smem, s>>>(p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, \
-                                                           scratch, vol, col_scale, partials, (int)p->nv,     \
-                                                           (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2],     \
-                                                           p->det00z, p->pv, p->flat_v, mode);                \
+        k_backproject<Z, PR><<<grid, p->bp_threads, smem, s>>>(p->d_cell_off, p->d_cell_ent, p->d_cols,       \
+                                                               p->d_invw, p->d_w, scratch, vol, col_scale,    \
+                                                               partials, (int)p->nv, (int)p->nz, (int)p->zs,  \
+                                                               p->lo[2], p->pitch[2], p->det00z, p->pv,       \
+                                                               p->flat_v, mode);                              \
     } while (0)
-    switch (p->bp_zpt) {
-        case 1: LAUNCH(1); break;
-        case 2: LAUNCH(2); break;
-        default: LAUNCH(4); break;
+    const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
+    switch (p->bp_zpt * 2 + (precise ? 1 : 0)) {
+        case 2: LAUNCH(1, false); break;
+        case 3: LAUNCH(1, true); break;
+        case 4: LAUNCH(2, false); break;
+        case 5: LAUNCH(2, true); break;
+        case 8: LAUNCH(4, false); break;
+        default: LAUNCH(4, true); break;
     }
 #undef LAUNCH
     CBCT_CHECK(cudaGetLastError());
