@@ -249,7 +249,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     t_a_loop = float(np.mean([s.elapsed_time(e) for s, e in ev["A"]]))
     t_at_loop = float(np.mean([s.elapsed_time(e) for s, e in ev["AT"]]))
     # kernel-only durations: CUDA events tight around the launches on this stream
-    scratch = torch.empty(op.m, dtype=torch.float32, device=dev)
+    scratch = op.new_bp_scratch()
 
     def kernel_ms(fn, reps=5):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

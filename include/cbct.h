@@ -26,7 +26,8 @@
  *     device-resident fan-beam tables of one (volume, trajectory) pair and all
  *     kernels run on caller-provided device buffers (torch-owned) in the
  *     internal layouts:
- *        volume:      [ny][nx][nz + 2*CBCT_ZPAD] fp32, z fastest, zero guard slices
+ *        volume:      [ny][nx][zs] fp32, z fastest, zs = round_up(nz + 2*CBCT_ZPAD, 4);
+ *                     slices [0,ZPAD) and [ZPAD+nz, zs) are zero guards
  *        projections: [n_views][nu][nv] fp32, v (detector row) fastest
  *     Launches are asynchronous on the given stream, never allocate, and are
  *     deterministic (no atomics on data).
@@ -74,8 +75,8 @@ typedef struct cbct_plan cbct_plan;
 typedef struct cbct_plan_info {
     int64_t n_voxels;          /* nx*ny*nz */
     int64_t n_rays;            /* n_views*nu*nv */
-    int64_t vol_elems;         /* padded internal volume length: ny*nx*(nz+2*CBCT_ZPAD) */
-    int64_t zstride;           /* nz + 2*CBCT_ZPAD */
+    int64_t vol_elems;         /* padded internal volume length: ny*nx*zstride */
+    int64_t zstride;           /* round_up(nz + 2*CBCT_ZPAD, 4) */
     int64_t n_columns;         /* n_views*nu detector columns */
     int64_t n_intervals;       /* column/cell intersections = nnz of the 2-D fan-beam matrix */
     int64_t max_intervals;     /* longest column list */
@@ -83,6 +84,9 @@ typedef struct cbct_plan_info {
     int64_t table_bytes;       /* device bytes held by the plan */
     int32_t proj_blocks;       /* number of fp64 partials written by cbct_project */
     int32_t bp_blocks;         /* number of fp64 partials written by cbct_backproject */
+    int64_t bp_scratch_floats; /* fp32 workspace cbct_backproject needs (scratch_proj) */
+    int32_t bp_fast_path;      /* 1: mode-1 A^T uses the boundary-form kernel */
+    int32_t pad_;
 } cbct_plan_info;
 
 /* ---- plan lifecycle ------------------------------------------------------ */
@@ -101,8 +105,8 @@ int cbct_project(const cbct_plan* plan, const float* vol, float* proj, double* n
 
 /* vol = A^T proj (mode 1, operator.py:328-341) or diag(A^T A) (mode 2,
  * operator.py:353-362; proj is ignored and may be NULL).  Every entry of vol,
- * guards included, is written (guards with 0).  scratch_proj: n_rays fp32 device
- * workspace (ray-length-weighted copy of proj).  If norm2_partials != NULL it
+ * guards included, is written (guards with 0).  scratch_proj: device workspace of
+ * info.bp_scratch_floats fp32 (per-column prefix sums of the ray-length-weighted proj).  If norm2_partials != NULL it
  * receives info.bp_blocks fp64 partials of vol^2.  If col_scale != NULL the
  * result is multiplied by col_scale (Jacobi chain applyT, solvers.py:178-181). */
 int cbct_backproject(const cbct_plan* plan, const float* proj, float* vol, int mode, float* scratch_proj,

@@ -18,6 +18,11 @@ c_i64, c_i32, c_f64, c_f32, c_p = ctypes.c_int64, ctypes.c_int32, ctypes.c_doubl
 CBCT_ZPAD = 4
 
 
+def zstride(nz: int) -> int:
+    """Padded z length of the device volume layout (include/cbct.h)."""
+    return (nz + 2 * CBCT_ZPAD + 3) // 4 * 4
+
+
 class CbctError(RuntimeError):
     """A libcbct call returned a non-zero status."""
 
@@ -37,6 +42,7 @@ class PlanInfo(ctypes.Structure):
         ("n_columns", c_i64), ("n_intervals", c_i64), ("max_intervals", c_i64),
         ("max_cell_entries", c_i64), ("table_bytes", c_i64),
         ("proj_blocks", c_i32), ("bp_blocks", c_i32),
+        ("bp_scratch_floats", c_i64), ("bp_fast_path", c_i32), ("pad_", c_i32),
     ]
 
 

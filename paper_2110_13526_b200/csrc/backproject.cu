@@ -44,7 +44,7 @@ __global__ void k_weight_rays(const ColumnHeader* __restrict__ cols, const doubl
 }
 
 template <int ZPT, bool PRECISE>
-__global__ void __launch_bounds__(512) k_backproject(const int64_t* __restrict__ cell_off,
+__global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ cell_off,
                                                      const CellEntry* __restrict__ cell_ent,
                                                      const ColumnHeader* __restrict__ cols,
                                                      const float* __restrict__ invw, const double* __restrict__ wtab,
@@ -135,10 +135,150 @@ __global__ void __launch_bounds__(512) k_backproject(const int64_t* __restrict__
             sq += (double)val * (double)val;
         }
     }
-    for (int k = threadIdx.x; k < CBCT_ZPAD; k += blockDim.x) {
-        out[k] = 0.0f;
-        out[CBCT_ZPAD + nz + k] = 0.0f;
+    for (int k = threadIdx.x; k < zs - nz; k += blockDim.x) out[k < CBCT_ZPAD ? k : nz + k] = 0.0f;  // guards
+    if (partials) {
+        const double tot = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = tot;
     }
+}
+
+
+// ---------------------------------------------------------------------------
+// Mode-1 fast path: boundary form.  For one crossing (column c, [t_a, t_b]) let
+// F_v(z) = |{t in [t_a,t_b] : z_v(t) < z}| be the part of ray v below height z.
+// The voxel [z_k, z_k+1) receives  G(z_k+1) - G(z_k)  with
+//   G(z) = sum_v yw_v F_v(z) = dt * P_c[V(z)] + yw_s F_s(z)
+// where V(z) counts the rays lying entirely below z (a prefix of v because rz_v
+// increases with v), P_c is the prefix sum of yw along v, and s = V(z) is the one
+// ray that can straddle z (segments are shorter than the ray spacing; the plan
+// checks this and otherwise uses k_bp_direct).  One lane per boundary; a warp
+// covers 32 boundaries = 31 voxels and exchanges G with its neighbour lane.
+
+// PY[c][v] = {P_c[v], yw[c][v]}, v = 0..nv (PY[c][nv] = {P_c[nv], 0});
+// yw = |r| * y; the flat row (if any) is kept out of P and stored in flatw[c].
+__global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
+                              const float* __restrict__ y, float2* __restrict__ py, float* __restrict__ flatw,
+                              int64_t n_cols, int nv, int flat_v) {
+    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= n_cols) return;
+    const float rxy2 = (float)cols[c].rxy2;
+    const float* yc = y + c * nv;
+    float2* pc = py + c * (int64_t)(nv + 1);
+    double carry = 0.0;
+    for (int base = 0; base < nv; base += 32) {
+        const int v = base + lane;
+        float yw = 0.0f;
+        if (v < nv) {
+            const float w = (float)wtab[v];
+            yw = sqrtf(fmaf(w, w, rxy2)) * yc[v];  // operator.py:102, 165
+            if (v == flat_v) {
+                flatw[c] = yw;
+                yw = 0.0f;
+            }
+        }
+        double incl = (double)yw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (v < nv) pc[v] = make_float2((float)(carry + incl - (double)yw), yw);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) pc[nv] = make_float2((float)carry, 0.0f);
+}
+
+template <int G, bool FLAT>
+__global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict__ cell_off,
+                                                      const CellEntry* __restrict__ cell_ent,
+                                                      const ColumnHeader* __restrict__ cols,
+                                                      const float* __restrict__ invw, const float2* __restrict__ py,
+                                                      const float* __restrict__ flatw, float* __restrict__ vol,
+                                                      const float* __restrict__ col_scale,
+                                                      double* __restrict__ partials, int nv, int nz, int zs,
+                                                      double lo2, double p2, double det00z, double pv) {
+    extern __shared__ float s_iw[];  // nv + 1 entries (s_iw[nv] = 0 pads the prefix end)
+    __shared__ float4 s_t0[kChunk], s_t1[kChunk];
+    __shared__ int s_vu[kChunk], s_fs[kChunk];
+    const int64_t cell = blockIdx.x;
+    const int64_t off = cell_off[cell];
+    const int ne = (int)(cell_off[cell + 1] - off);
+    for (int k = threadIdx.x; k <= nv; k += blockDim.x) s_iw[k] = k < nv ? invw[k] : 0.0f;
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    float z[G], acc[G], sgn[G];
+    int kb[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        kb[g] = (warp + g * nwarps) * 31 + lane;  // boundary index (voxel below it is kb-1)
+        z[g] = (float)(lo2 + (double)kb[g] * p2);
+        acc[g] = 0.0f;
+        sgn[g] = z[g] >= 0.0f ? 1.0f : 0.0f;
+    }
+    // Row coordinate of a ray through height z at parameter t: v = z/(t pv) + c0,
+    // c0 = -det00z/pv (= nv/2 - 1/2 without a principal-point offset).  c0 is split
+    // into an integer and a fraction so the fp32 FFMA only carries z/(t pv) + frac:
+    // its rounding then scales with |rz| of the rays near the boundary instead of
+    // with |c0| (which would misclassify near-mid-plane rays by ~1e-5 pixel).
+    const double c0d = -det00z / pv;
+    const double c0i = floor(c0d + 0.5);
+    const float c0f = (float)(c0d - c0i);
+    const int magic = 0x4B400000 - (int)c0i - 1;  // floor(W) + c0i + 1 via the 1.5*2^23 trick
+    const float wlo = (float)(-c0i - 1.0), whi = (float)((double)nv - c0i - 0.5);
+    const float fpv = (float)pv;
+    const float2* __restrict__ pyb = py;
+
+    for (int base = 0; base < ne; base += kChunk) {
+        const int nch = min(kChunk, ne - base);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nch; k += blockDim.x) {
+            const CellEntry ce = cell_ent[off + base + k];
+            const ColumnHeader& h = cols[ce.vu];
+            const float ta = ce.tau_a, tb = ce.tau_b, tr = h.t_ref;
+            s_t0[k] = make_float4(ta, tb, tr, tb - ta);
+            s_t1[k] = make_float4(1.0f / ((ta + tr) * fpv), 1.0f / ((tb + tr) * fpv), FLAT ? flatw[ce.vu] : 0.0f, 0.0f);
+            s_vu[k] = ce.vu;
+            s_fs[k] = FLAT ? h.flat_slab : 0;
+        }
+        __syncthreads();
+        for (int k = 0; k < nch; ++k) {
+            const float4 t0 = s_t0[k], t1 = s_t1[k];
+            const float2* __restrict__ pyc = pyb + (int64_t)s_vu[k] * (nv + 1);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float ip = sgn[g] != 0.0f ? t1.y : t1.x;  // t* = t_b above the mid-plane, t_a below
+                float W = fmaf(z[g], ip, c0f);
+                W = fminf(fmaxf(W, wlo), whi);  // keeps floor(W) + c0i + 1 in [0, nv]
+                const int vh = __float_as_int(__fadd_rd(W, 12582912.0f)) - magic;
+                const float2 pv2 = __ldg(pyc + vh);
+                const float iw = s_iw[vh];
+                const float u = fmaf(z[g], iw, -t0.z);  // tau of z on the straddling ray
+                const bool neg = iw < 0.0f;
+                const float lo = neg ? fmaxf(u, t0.x) : t0.x;
+                const float hi = neg ? t0.y : fminf(u, t0.y);
+                const float F = fmaxf(hi - lo, 0.0f);
+                float Gv = fmaf(F, pv2.y, t0.w * pv2.x);
+                const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
+                acc[g] += Gn - Gv;
+                if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.z : 0.0f;
+            }
+        }
+    }
+
+    float* out = vol + cell * zs;
+    double sq = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int iz = kb[g];  // voxel [z_kb, z_kb+1)
+        if (lane < 31 && iz < nz) {
+            float val = acc[g];
+            if (col_scale) val *= col_scale[cell * zs + CBCT_ZPAD + iz];
+            out[CBCT_ZPAD + iz] = val;
+            sq += (double)val * (double)val;
+        }
+    }
+    for (int k = threadIdx.x; k < zs - nz; k += blockDim.x) out[k < CBCT_ZPAD ? k : nz + k] = 0.0f;  // guards
     if (partials) {
         const double tot = block_sum(sq);
         if (threadIdx.x == 0) partials[blockIdx.x] = tot;
@@ -153,6 +293,39 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
     if (mode != 1 && mode != 2) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode must be 1 or 2");
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode 1 needs projections");
     cudaStream_t s = (cudaStream_t)stream;
+    const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
+    if (mode == 1 && p->bp_boundary_ok && !precise) {
+        float2* pyb = reinterpret_cast<float2*>(scratch);
+        float* flatw = scratch + 2 * p->n_cols * (p->nv + 1);
+        const int64_t nthreads = p->n_cols * 32;
+        k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
+                                                                           p->n_cols, (int)p->nv, p->flat_v);
+        CBCT_CHECK(cudaGetLastError());
+        const size_t smem = (size_t)(p->nv + 1) * sizeof(float);
+        const dim3 grid((unsigned)p->n_cells);
+#define LAUNCH_G(G, FL)                                                                                        \
+        do {                                                                                                   \
+            if (smem > 16 * 1024)                                                                              \
+                CBCT_CHECK(cudaFuncSetAttribute(k_bp_boundary<G, FL>,                                          \
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+            k_bp_boundary<G, FL><<<grid, p->bpg_threads, smem, s>>>(                                           \
+                p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
+                (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv);                  \
+        } while (0)
+        const bool fl = p->flat_v >= 0;
+        switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
+            case 2: LAUNCH_G(1, false); break;
+            case 3: LAUNCH_G(1, true); break;
+            case 4: LAUNCH_G(2, false); break;
+            case 5: LAUNCH_G(2, true); break;
+            case 8: LAUNCH_G(4, false); break;
+            default: LAUNCH_G(4, true); break;
+        }
+#undef LAUNCH_G
+        CBCT_CHECK(cudaGetLastError());
+        cbct_count_launch(2);
+        return 0;
+    }
     const int64_t nr = p->n_rays;
     k_weight_rays<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, mode == 1 ? proj : nullptr,
                                                                  scratch, p->n_cols, (int)p->nv);
@@ -162,15 +335,14 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
 #define LAUNCH(Z, PR)                                                                                         \
     do {                                                                                                      \
         if (smem > 40 * 1024)                                                                                 \
-            CBCT_CHECK(cudaFuncSetAttribute(k_backproject<Z, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+            CBCT_CHECK(cudaFuncSetAttribute(k_bp_direct<Z, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                             (int)smem));                                                      \
-        k_backproject<Z, PR><<<grid, p->bp_threads, smem, s>>>(p->d_cell_off, p->d_cell_ent, p->d_cols,       \
-                                                               p->d_invw, p->d_w, scratch, vol, col_scale,    \
-                                                               partials, (int)p->nv, (int)p->nz, (int)p->zs,  \
-                                                               p->lo[2], p->pitch[2], p->det00z, p->pv,       \
-                                                               p->flat_v, mode);                              \
+        k_bp_direct<Z, PR><<<grid, p->bp_threads, smem, s>>>(p->d_cell_off, p->d_cell_ent, p->d_cols,         \
+                                                             p->d_invw, p->d_w, scratch, vol, col_scale,      \
+                                                             partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
+                                                             p->lo[2], p->pitch[2], p->det00z, p->pv,         \
+                                                             p->flat_v, mode);                                \
     } while (0)
-    const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
     switch (p->bp_zpt * 2 + (precise ? 1 : 0)) {
         case 2: LAUNCH(1, false); break;
         case 3: LAUNCH(1, true); break;

@@ -110,7 +110,9 @@ extern "C" int cbct_ref_backproject(const double* proj, double* out, const doubl
     const int64_t n = n0 * n1 * n2, m = V * nu * nv;
     DevBuf d_in, d_proj, d_scr, d_vol, d_out;
     CBCT_CHECK(cudaMalloc(&d_proj.p, m * sizeof(float)));
-    CBCT_CHECK(cudaMalloc(&d_scr.p, m * sizeof(float)));
+    cbct_plan_info info;
+    cbct_plan_get_info(p, &info);
+    CBCT_CHECK(cudaMalloc(&d_scr.p, info.bp_scratch_floats * sizeof(float)));
     CBCT_CHECK(cudaMalloc(&d_vol.p, p->vol_elems * sizeof(float)));
     CBCT_CHECK(cudaMalloc(&d_out.p, n * sizeof(double)));
     if (mode == 1) {

@@ -1,7 +1,7 @@
 // cbct_internal.cuh -- private types and helpers of libcbct.so (sm_100a).
 //
 // Data layout in HBM:
-//   volume      [ny][nx][zs]   fp32, zs = nz + 2*CBCT_ZPAD, z fastest; slices
+//   volume      [ny][nx][zs]   fp32, zs = round_up(nz + 2*CBCT_ZPAD, 4), z fastest; slices
 //                              [0,ZPAD) and [ZPAD+nz, zs) are zero guards
 //   projections [V][nu][nv]    fp32, detector row v fastest
 //   column table (A):    per detector column c = view*nu + u, entries
@@ -61,7 +61,11 @@ struct cbct_plan {
     float* d_invw = nullptr;        // per-row 1/rz (fp32; +-1e30 for flat rows), nv
     // launch shapes
     int proj_threads, proj_rpt;
+    int proj_tma, proj_tma_k, proj_tma_stages;  // TMA-staged projector shape
     int bp_threads, bp_zpt;
+    int bpg_threads, bpg_groups;  // boundary-form backprojector shape
+    bool bp_boundary_ok;          // at most one ray straddles any voxel boundary per crossing
+    float max_dtau;               // longest column/cell interval (ray parameter)
     int32_t proj_blocks, bp_blocks;
 };
 

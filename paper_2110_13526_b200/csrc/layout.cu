@@ -52,10 +52,11 @@ __global__ void k_transpose_back(const Tin* __restrict__ in, Tout* __restrict__ 
 }
 
 __global__ void k_zero_guards(float* vol, int64_t n_cells, int64_t zs, int64_t nz) {
+    const int64_t ng = zs - nz;  // guard slots per cell column
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_cells * 2 * CBCT_ZPAD) return;
-    const int64_t cell = i / (2 * CBCT_ZPAD);
-    const int k = (int)(i - cell * 2 * CBCT_ZPAD);
+    if (i >= n_cells * ng) return;
+    const int64_t cell = i / ng;
+    const int64_t k = i - cell * ng;
     vol[cell * zs + (k < CBCT_ZPAD ? k : nz + k)] = 0.0f;
 }
 
@@ -88,7 +89,7 @@ extern "C" int cbct_volume_to_internal(const cbct_plan* p, const void* src, int 
     int rc = f64 ? launch_t((const double*)src, dst, p->nz, cells, p->zs, CBCT_ZPAD, 1, 0, 0, s)
                  : launch_t((const float*)src, dst, p->nz, cells, p->zs, CBCT_ZPAD, 1, 0, 0, s);
     if (rc) return rc;
-    const int64_t ng = cells * 2 * CBCT_ZPAD;
+    const int64_t ng = cells * (p->zs - p->nz);
     k_zero_guards<<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(dst, cells, p->zs, p->nz);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();

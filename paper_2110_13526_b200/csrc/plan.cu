@@ -14,6 +14,7 @@
 // resulting fp32 tables.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -204,6 +205,21 @@ __global__ void k_max_span(const int64_t* off, int64_t n, unsigned long long* ou
     atomicMax(out, (unsigned long long)(off[k + 1] - off[k]));
 }
 
+__global__ void k_max_dtau(const float2* ent, const int64_t* col_off, const ColumnHeader* cols, int64_t n_cols,
+                           unsigned int* out_bits, unsigned int* out_tmin) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    const int64_t a = col_off[c], b = col_off[c + 1];
+    if (a == b) return;
+    float prev = cols[c].tau_start, mx = 0.0f;
+    for (int64_t k = a; k < b; ++k) {
+        mx = fmaxf(mx, ent[k].x - prev);
+        prev = ent[k].x;
+    }
+    atomicMax(out_bits, __float_as_uint(mx));  // non-negative floats order like their bit patterns
+    atomicMin(out_tmin, __float_as_uint((float)cols[c].tmin));  // tmin >= 0: bit order == value order
+}
+
 __global__ void k_row_tables(int64_t nv, double det00z, double pv, double p2, double* w, float* invw) {
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= nv) return;
@@ -252,7 +268,7 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: counts must be >= 1");
     if (!(g->pitch[0] > 0 && g->pitch[1] > 0 && g->pitch[2] > 0))
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: voxel pitch must be > 0");
-    const int64_t zs = g->nz + 2 * CBCT_ZPAD;
+    const int64_t zs = (g->nz + 2 * CBCT_ZPAD + 3) / 4 * 4;  // 16-B aligned cell columns (TMA)
     if (g->nx * g->ny * zs >= (int64_t)INT32_MAX)
         return cbct_fail(CBCT_E_GEOMETRY, "volume too large for 32-bit cell offsets on one device");
     const int64_t V = g->n_views;
@@ -364,6 +380,26 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         unsigned long long mx[2];
         TRYC(cudaMemcpyAsync(mx, d_max, sizeof(mx), cudaMemcpyDeviceToHost, stream));
 
+        {
+            // straddle bound for the boundary-form backprojector (backproject.cu)
+            unsigned int* d_bits = nullptr;
+            TRYC(cudaMalloc(&d_bits, 2 * sizeof(unsigned int)));
+            unsigned int init[2] = {0u, 0x7f7fffffu};
+            TRYC(cudaMemcpyAsync(d_bits, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+            k_max_dtau<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(p->d_col_ent, p->d_col_off, p->d_cols,
+                                                                       p->n_cols, d_bits, d_bits + 1);
+            unsigned int hb[2];
+            TRYC(cudaMemcpyAsync(hb, d_bits, sizeof(hb), cudaMemcpyDeviceToHost, stream));
+            TRYC(cudaStreamSynchronize(stream));
+            cudaFree(d_bits);
+            float mx, tmin_f;
+            memcpy(&mx, &hb[0], 4);
+            memcpy(&tmin_f, &hb[1], 4);
+            p->max_dtau = mx;
+            const double wmax = fmax(fabs(det00z), fabs(det00z + (double)(g->nv - 1) * pv));
+            // two rays can straddle one boundary only if |w| dt > pv t_a somewhere
+            p->bp_boundary_ok = wmax * (double)mx < 0.9 * pv * (double)tmin_f;
+        }
         TRY(dev_alloc(&p->d_w, g->nv, &total));
         TRY(dev_alloc(&p->d_invw, g->nv, &total));
         k_row_tables<<<blocks_for(g->nv, 128), 128, 0, stream>>>(g->nv, det00z, pv, g->pitch[2], p->d_w, p->d_invw);
@@ -377,9 +413,24 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     p->proj_rpt = g->nv <= 512 ? 1 : (g->nv <= 1024 ? 2 : 4);
     p->proj_threads = (int)(((g->nv + p->proj_rpt - 1) / p->proj_rpt + 31) / 32 * 32);
     p->proj_blocks = (int32_t)p->n_cols;
+    {
+        // ring of ~32 KB of cell columns, stages of K intervals (project.cu k_project_tma)
+        const int64_t col_bytes = zs * 4;
+        const int64_t ring_cols = std::max<int64_t>(8, 32768 / col_bytes);
+        p->proj_tma_k = ring_cols >= 16 ? 4 : 2;
+        p->proj_tma_stages = (int)std::min<int64_t>(16, std::max<int64_t>(3, ring_cols / p->proj_tma_k));
+        const int64_t smem = 16 * ((2 * p->proj_tma_stages * 8 + 15) / 16) + (p->max_intervals + 4) * 8 +
+                             (int64_t)p->proj_tma_stages * p->proj_tma_k * col_bytes;
+        p->proj_tma = smem <= 200 * 1024 ? 1 : 0;
+    }
     p->bp_zpt = g->nz <= 512 ? 1 : (g->nz <= 1024 ? 2 : 4);
     p->bp_threads = (int)(((g->nz + p->bp_zpt - 1) / p->bp_zpt + 31) / 32 * 32);
     p->bp_blocks = (int32_t)p->n_cells;
+    {
+        const int64_t warps = (g->nz + 30) / 31;  // 31 voxels per warp (32 boundaries)
+        p->bpg_groups = warps <= 32 ? 1 : (warps <= 64 ? 2 : 4);
+        p->bpg_threads = (int)(((warps + p->bpg_groups - 1) / p->bpg_groups) * 32);
+    }
     p->table_bytes = total;
     cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
@@ -407,6 +458,8 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->max_cell_entries = p->max_cell_entries;
     info->table_bytes = (int64_t)p->table_bytes;
     info->proj_blocks = p->proj_blocks;
+    info->bp_scratch_floats = 2 * p->n_cols * (p->nv + 1) + p->n_cols;
+    info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
     info->bp_blocks = p->bp_blocks;
     return 0;
 }

@@ -15,9 +15,11 @@
 // loop.  Lanes of a warp are consecutive rows v, so vol[cell, iz] loads are
 // coalesced along z (the internal volume layout is z-fastest).
 #include <cmath>
+#include <cstdlib>
 
 #include "cbct_internal.cuh"
 #include "reduce.cuh"
+#include "tma.cuh"
 
 namespace {
 
@@ -65,6 +67,24 @@ __device__ __forceinline__ void ray_setup(RayState& s, const ColumnHeader& h, in
     s.tz = s.kf > 0.0f ? s.tz0 : INFINITY;
 }
 
+// One interval of the column walk for one ray.  `idx` is the guard-padded
+// element index cell_base + iz, kept in 32 bits so the address is a single
+// IMAD.WIDE.U32 off the uniform volume pointer.
+__device__ __forceinline__ void interval_step(RayState& s, const float* __restrict__ vol, float bn, int cell,
+                                              float dl) {
+    const uint32_t idx = (uint32_t)(cell + s.iz);
+    float val = __ldg(vol + idx);
+    s.acc = fmaf(dl, val, s.acc);
+    while (s.tz < bn) {  // z-plane crossing inside this interval (rare per lane)
+        const float v2 = __ldg(vol + (uint32_t)(cell + s.iz + s.dz));
+        s.acc = fmaf(bn - s.tz, v2 - val, s.acc);
+        val = v2;
+        s.iz += s.dz;
+        s.jf += 1.0f;
+        s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
+    }
+}
+
 template <int RPT>
 __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict__ cols,
                                                  const int64_t* __restrict__ col_off,
@@ -72,12 +92,15 @@ __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict_
                                                  const float* __restrict__ vol, float* __restrict__ proj,
                                                  double* __restrict__ partials, int nv, int nz, double lo2,
                                                  double p2, int flat_v) {
-    extern __shared__ float2 s_ent[];
+    extern __shared__ float4 s_ent4[];  // column entries, two per float4, padded to an even count
+    float2* s_ent = reinterpret_cast<float2*>(s_ent4);
     const int64_t c = blockIdx.x;
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
     for (int k = threadIdx.x; k < M; k += blockDim.x) s_ent[k] = col_ent[off + k];
+    // odd count: pad with a zero-length interval (cell 0, reads a valid zero-weight element)
+    if (threadIdx.x == 0 && (M & 1)) s_ent[M] = make_float2(col_ent[off + M - 1].x, __int_as_float(0));
 
     RayState st[RPT];
 #pragma unroll
@@ -85,26 +108,18 @@ __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict_
     __syncthreads();
 
     float a = h.tau_start;
-    for (int m = 0; m < M; ++m) {
-        const float2 e = s_ent[m];
-        const float bn = e.x;
-        const float* __restrict__ colp = vol + __float_as_int(e.y);
-        const float dl = bn - a;
+    const int M2 = (M + 1) >> 1;
+    for (int m2 = 0; m2 < M2; ++m2) {
+        const float4 e = s_ent4[m2];  // {tau_end0, cell0, tau_end1, cell1}
+        const float dl0 = e.x - a;
+        const float dl1 = e.z - e.x;  // 0 for the pad entry (tau_end1 == tau_end0)
+        const int c0 = __float_as_int(e.y), c1 = __float_as_int(e.w);
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-            RayState& s = st[r];
-            float val = __ldg(colp + s.iz);
-            s.acc = fmaf(dl, val, s.acc);
-            while (s.tz < bn) {  // z-plane crossing inside this interval
-                const float v2 = __ldg(colp + s.iz + s.dz);
-                s.acc = fmaf(bn - s.tz, v2 - val, s.acc);
-                val = v2;
-                s.iz += s.dz;
-                s.jf += 1.0f;
-                s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
-            }
+            interval_step(st[r], vol, e.x, c0, dl0);
+            interval_step(st[r], vol, e.z, c1, dl1);
         }
-        a = bn;
+        a = e.z;
     }
 
     double sq = 0.0;
@@ -125,13 +140,157 @@ __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict_
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// TMA-staged variant.  A producer warp streams the z column of every upcoming
+// cell of this detector column (zs contiguous floats, 16-B aligned) into a
+// shared-memory ring with cp.async.bulk; full/empty mbarriers hand stages of K
+// intervals to the ray warps, which then read the volume with LDS instead of
+// waiting ~L2 latency on each LDG.
+__device__ __forceinline__ void interval_step_smem(RayState& s, const float* __restrict__ colp, float bn, float dl) {
+    float val = colp[s.iz];
+    s.acc = fmaf(dl, val, s.acc);
+    while (s.tz < bn) {
+        const float v2 = colp[s.iz + s.dz];
+        s.acc = fmaf(bn - s.tz, v2 - val, s.acc);
+        val = v2;
+        s.iz += s.dz;
+        s.jf += 1.0f;
+        s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
+    }
+}
+
+template <int RPT, int K>
+__global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restrict__ cols,
+                                                     const int64_t* __restrict__ col_off,
+                                                     const float2* __restrict__ col_ent,
+                                                     const double* __restrict__ wtab, const float* __restrict__ vol,
+                                                     float* __restrict__ proj, double* __restrict__ partials, int nv,
+                                                     int nz, int zs, double lo2, double p2, int flat_v, int nstages,
+                                                     int ent_cap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t* empty = full + nstages;
+    float4* s_ent4 = reinterpret_cast<float4*>(smem_raw + 16 * ((2 * nstages * 8 + 15) / 16));
+    float2* s_ent = reinterpret_cast<float2*>(s_ent4);
+    float* ring = reinterpret_cast<float*>(s_ent4 + ent_cap / 2);
+    const int nwc = (blockDim.x >> 5) - 1;  // consumer warps; the last warp produces
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = warp == nwc;
+
+    const int64_t c = blockIdx.x;
+    const ColumnHeader h = cols[c];
+    const int64_t off = col_off[c];
+    const int M = (int)(col_off[c + 1] - off);
+    for (int k = threadIdx.x; k < M; k += blockDim.x) s_ent[k] = col_ent[off + k];
+    if (threadIdx.x == 0) {
+        if (M & 1) s_ent[M] = make_float2(col_ent[off + M - 1].x, __int_as_float(0));
+        for (int i = 0; i < nstages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], nwc);
+        }
+        mbar_fence_init();
+    }
+    RayState st[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+        ray_setup(st[r], h, producer ? nv : threadIdx.x + r * nwc * 32, nv, wtab, lo2, p2, nz, flat_v);
+    __syncthreads();
+
+    const int nst = (M + K - 1) / K;  // stages of K intervals
+    const uint32_t col_bytes = (uint32_t)zs * 4u;
+    if (producer) {
+        if (lane == 0) {
+            for (int i = 0; i < nst; ++i) {
+                const int slot = i % nstages, round = i / nstages;
+                if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+                const int m0 = i * K, cnt = min(K, M - m0);
+                mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
+                float* dst = ring + (size_t)slot * K * zs;
+                for (int j = 0; j < cnt; ++j)
+                    bulk_g2s(dst + j * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + j].y), col_bytes, &full[slot]);
+            }
+        }
+    } else {
+        float a = h.tau_start;
+        for (int i = 0; i < nst; ++i) {
+            const int slot = i % nstages, round = i / nstages;
+            mbar_wait(&full[slot], round & 1);
+            const float* stage = ring + (size_t)slot * K * zs;
+            const int m0 = i * K;
+#pragma unroll
+            for (int j = 0; j < K; j += 2) {
+                if (m0 + j >= M) break;
+                const float4 e = s_ent4[(m0 + j) >> 1];
+                const float dl0 = e.x - a, dl1 = e.z - e.x;
+                const float* c0p = stage + j * zs;
+                const float* c1p = (m0 + j + 1 < M) ? c0p + zs : c0p;  // pad entry: zero-length, any column
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    interval_step_smem(st[r], c0p, e.x, dl0);
+                    interval_step_smem(st[r], c1p, e.z, dl1);
+                }
+                a = e.z;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+    }
+
+    double sq = 0.0;
+    if (!producer) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int v = threadIdx.x + r * nwc * 32;
+            if (v < nv) {
+                const double w = wtab[v];
+                const float raylen = (float)sqrt(h.rxy2 + w * w);
+                const float out = st[r].acc * raylen;
+                proj[c * nv + v] = out;
+                sq += (double)out * (double)out;
+            }
+        }
+    }
+    if (partials) {
+        const double tot = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+    }
+}
+
 }  // namespace
 
 extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, double* partials, void* stream) {
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project: null argument");
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t smem = (size_t)(p->max_intervals > 0 ? p->max_intervals : 1) * sizeof(float2);
     const dim3 grid((unsigned)p->n_cols);
+    if (p->proj_tma && getenv("CBCT_PROJ_LDG") == nullptr) {
+        const int K = p->proj_tma_k, ns = p->proj_tma_stages;
+        const int ent_cap = (int)((p->max_intervals + 2 + 1) / 2 * 2);
+        const size_t smem = 16 * ((2 * ns * 8 + 15) / 16) + (size_t)ent_cap * sizeof(float2) +
+                            (size_t)ns * K * p->zs * sizeof(float);
+        const int nt = p->proj_threads + 32;
+#define LAUNCH_T(R, KK)                                                                                        \
+        do {                                                                                                   \
+            CBCT_CHECK(cudaFuncSetAttribute(k_project_tma<R, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                            (int)smem));                                                       \
+            k_project_tma<R, KK><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol,      \
+                                                        proj, partials, (int)p->nv, (int)p->nz, (int)p->zs,      \
+                                                        p->lo[2], p->pitch[2], p->flat_v, ns, ent_cap);          \
+        } while (0)
+        switch (p->proj_rpt * 10 + K) {
+            case 12: LAUNCH_T(1, 2); break;
+            case 14: LAUNCH_T(1, 4); break;
+            case 22: LAUNCH_T(2, 2); break;
+            case 24: LAUNCH_T(2, 4); break;
+            case 42: LAUNCH_T(4, 2); break;
+            default: LAUNCH_T(4, 4); break;
+        }
+#undef LAUNCH_T
+        CBCT_CHECK(cudaGetLastError());
+        cbct_count_launch();
+        return 0;
+    }
+    const size_t smem = (size_t)(p->max_intervals + 2) * sizeof(float2);
     const int nt = p->proj_threads;
 #define LAUNCH(R)                                                                                            \
     do {                                                                                                     \

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import CBCT_ZPAD, call
+from ._lib import CBCT_ZPAD, call, zstride
 from .geometry import TrajectoryGeometry, VolumeGeometry, geometry_key, view_tables
 from .phantom import Volume, coerce_data
 
@@ -66,7 +66,7 @@ class InternalVolume:
 
     def as_3d(self):
         g = self.geometry
-        zs = g.nz + 2 * CBCT_ZPAD
+        zs = zstride(g.nz)
         return self.data.view(g.ny, g.nx, zs)[:, :, CBCT_ZPAD:CBCT_ZPAD + g.nz].permute(2, 0, 1)
 
 
@@ -162,6 +162,10 @@ class CbctOperator:
     def new_volume(self) -> torch.Tensor:
         return torch.zeros(self.vol_elems, dtype=torch.float32, device=self.device)
 
+    def new_bp_scratch(self) -> torch.Tensor:
+        """Workspace of cbct_backproject (per-column prefix sums)."""
+        return torch.empty(int(self.info.bp_scratch_floats), dtype=torch.float32, device=self.device)
+
     def new_projections(self) -> torch.Tensor:
         return torch.zeros(self.m, dtype=torch.float32, device=self.device)
 
@@ -213,7 +217,7 @@ class CbctOperator:
     def backproject_internal(self, y, out: torch.Tensor, mode: int = 1, norm2: bool = False, col_scale=None,
                              scratch=None):
         """out = A^T y (mode 1) or diag(A^T A) (mode 2, y ignored); ||out||^2 if norm2."""
-        scratch = torch.empty(self.m, dtype=torch.float32, device=self.device) if scratch is None else scratch
+        scratch = self.new_bp_scratch() if scratch is None else scratch
         part = self._partials if norm2 else None
         call("cbct_backproject", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode), _ptr(scratch),
              _ptr(col_scale), _ptr(part), self._stream())

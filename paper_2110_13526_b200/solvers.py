@@ -222,7 +222,7 @@ class _Chain:
 
     def _scratch(self):
         if not hasattr(self, "_scr"):
-            self._scr = torch.empty(self.op.m, dtype=torch.float32, device=self.dev.device)
+            self._scr = self.op.new_bp_scratch()
         return self._scr
 
     def z_of(self, x0):
