@@ -31,6 +31,22 @@ struct Tri {  // staged per-crossing data
 
 constexpr int kChunk = 256;
 
+// Cells are visited in 16x16 tiles so concurrently resident CTAs share the
+// detector columns they read (L2 locality of the prefix arrays).
+__device__ __forceinline__ int64_t tiled_cell(int64_t b, int nx, int ny) {
+    const int T = 16;
+    const int tx = (nx + T - 1) / T;
+    const int64_t per_tile = (int64_t)T * T;
+    const int64_t tile = b / per_tile;
+    const int k = (int)(b - tile * per_tile);
+    const int ty0 = (int)(tile / tx) * T, tx0 = (int)(tile % tx) * T;
+    // cells of partial edge tiles are packed by skipping out-of-range slots in the host-computed grid
+    const int iy = ty0 + k / T, ix = tx0 + k % T;
+    if (ix >= nx || iy >= ny) return -1;
+    return (int64_t)iy * nx + ix;
+}
+
+
 // yw[c, v] = |r(c, v)| * y[c, v]  (y == NULL -> |r|)   operator.py:102
 __global__ void k_weight_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
                               const float* __restrict__ y, float* __restrict__ yw, int64_t n_cols, int nv) {
@@ -52,10 +68,14 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
                                                      float* __restrict__ vol, const float* __restrict__ col_scale,
                                                      double* __restrict__ partials, int nv, int nz, int zs,
                                                      double lo2, double p2, double det00z, double pv, int flat_v,
-                                                     int mode) {
+                                                     int mode, int nx, int ny) {
     extern __shared__ float s_invw[];
     __shared__ Tri s_tri[kChunk];
-    const int64_t cell = blockIdx.x;
+    const int64_t cell = tiled_cell(blockIdx.x, nx, ny);
+    if (cell < 0) {  // padding slot of an edge tile
+        if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
+        return;
+    }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
     for (int k = threadIdx.x; k < nv; k += blockDim.x) s_invw[k] = invw[k];
@@ -154,17 +174,20 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
 // checks this and otherwise uses k_bp_direct).  One lane per boundary; a warp
 // covers 32 boundaries = 31 voxels and exchanges G with its neighbour lane.
 
-// PY[c][v] = {P_c[v], yw[c][v]}, v = 0..nv (PY[c][nv] = {P_c[nv], 0});
-// yw = |r| * y; the flat row (if any) is kept out of P and stored in flatw[c].
+// P[c][v] = sum_{v' < v} yw[c][v'], v = 0..nv+1 (P[c][nv+1] = P[c][nv]); yw = |r| * y.
+// The straddling ray's own weight is recovered as P[v+1] - P[v] (it only scales
+// the straddle fraction F, so the fp32 cancellation there is harmless), which
+// halves the bytes per boundary lookup.  The flat row (if any) is kept out of P
+// and stored in flatw[c].
 __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
-                              const float* __restrict__ y, float2* __restrict__ py, float* __restrict__ flatw,
+                              const float* __restrict__ y, float* __restrict__ pref, float* __restrict__ flatw,
                               int64_t n_cols, int nv, int flat_v) {
     const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (c >= n_cols) return;
     const float rxy2 = (float)cols[c].rxy2;
     const float* yc = y + c * nv;
-    float2* pc = py + c * (int64_t)(nv + 1);
+    float* pc = pref + c * (int64_t)(nv + 2);
     double carry = 0.0;
     for (int base = 0; base < nv; base += 32) {
         const int v = base + lane;
@@ -183,25 +206,30 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
             const double t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (v < nv) pc[v] = make_float2((float)(carry + incl - (double)yw), yw);
+        if (v < nv) pc[v] = (float)(carry + incl - (double)yw);
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) pc[nv] = make_float2((float)carry, 0.0f);
+    if (lane == 0) pc[nv] = pc[nv + 1] = (float)carry;
 }
 
 template <int G, bool FLAT>
 __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict__ cell_off,
                                                       const CellEntry* __restrict__ cell_ent,
                                                       const ColumnHeader* __restrict__ cols,
-                                                      const float* __restrict__ invw, const float2* __restrict__ py,
+                                                      const float* __restrict__ invw, const float* __restrict__ pref,
                                                       const float* __restrict__ flatw, float* __restrict__ vol,
                                                       const float* __restrict__ col_scale,
                                                       double* __restrict__ partials, int nv, int nz, int zs,
-                                                      double lo2, double p2, double det00z, double pv) {
+                                                      double lo2, double p2, double det00z, double pv, int nx,
+                                                      int ny) {
     extern __shared__ float s_iw[];  // nv + 1 entries (s_iw[nv] = 0 pads the prefix end)
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
-    const int64_t cell = blockIdx.x;
+    const int64_t cell = tiled_cell(blockIdx.x, nx, ny);
+    if (cell < 0) {  // padding slot of an edge tile
+        if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
+        return;
+    }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
     for (int k = threadIdx.x; k <= nv; k += blockDim.x) s_iw[k] = k < nv ? invw[k] : 0.0f;
@@ -227,7 +255,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     const int magic = 0x4B400000 - (int)c0i - 1;  // floor(W) + c0i + 1 via the 1.5*2^23 trick
     const float wlo = (float)(-c0i - 1.0), whi = (float)((double)nv - c0i - 0.5);
     const float fpv = (float)pv;
-    const float2* __restrict__ pyb = py;
+    const float* __restrict__ pyb = pref;
 
     for (int base = 0; base < ne; base += kChunk) {
         const int nch = min(kChunk, ne - base);
@@ -244,21 +272,21 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         __syncthreads();
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float2* __restrict__ pyc = pyb + (int64_t)s_vu[k] * (nv + 1);
+            const float* __restrict__ pyc = pyb + (int64_t)s_vu[k] * (nv + 2);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const float ip = sgn[g] != 0.0f ? t1.y : t1.x;  // t* = t_b above the mid-plane, t_a below
                 float W = fmaf(z[g], ip, c0f);
                 W = fminf(fmaxf(W, wlo), whi);  // keeps floor(W) + c0i + 1 in [0, nv]
                 const int vh = __float_as_int(__fadd_rd(W, 12582912.0f)) - magic;
-                const float2 pv2 = __ldg(pyc + vh);
+                const float P0 = __ldg(pyc + vh), P1 = __ldg(pyc + vh + 1);
                 const float iw = s_iw[vh];
                 const float u = fmaf(z[g], iw, -t0.z);  // tau of z on the straddling ray
                 const bool neg = iw < 0.0f;
                 const float lo = neg ? fmaxf(u, t0.x) : t0.x;
                 const float hi = neg ? t0.y : fminf(u, t0.y);
                 const float F = fmaxf(hi - lo, 0.0f);
-                float Gv = fmaf(F, pv2.y, t0.w * pv2.x);
+                float Gv = fmaf(F, P1 - P0, t0.w * P0);
                 const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
                 acc[g] += Gn - Gv;
                 if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.z : 0.0f;
@@ -295,14 +323,15 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
     cudaStream_t s = (cudaStream_t)stream;
     const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
     if (mode == 1 && p->bp_boundary_ok && !precise) {
-        float2* pyb = reinterpret_cast<float2*>(scratch);
-        float* flatw = scratch + 2 * p->n_cols * (p->nv + 1);
+        float* pyb = scratch;
+        float* flatw = scratch + p->n_cols * (p->nv + 2);
         const int64_t nthreads = p->n_cols * 32;
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v);
         CBCT_CHECK(cudaGetLastError());
         const size_t smem = (size_t)(p->nv + 1) * sizeof(float);
-        const dim3 grid((unsigned)p->n_cells);
+        const int64_t tiles = ((p->nx + 15) / 16) * ((p->ny + 15) / 16);
+        const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \
         do {                                                                                                   \
             if (smem > 16 * 1024)                                                                              \
@@ -310,7 +339,8 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
             k_bp_boundary<G, FL><<<grid, p->bpg_threads, smem, s>>>(                                           \
                 p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
-                (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv);                  \
+                (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,      \
+                (int)p->ny);                                                                                   \
         } while (0)
         const bool fl = p->flat_v >= 0;
         switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
@@ -331,7 +361,7 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                                                                  scratch, p->n_cols, (int)p->nv);
     CBCT_CHECK(cudaGetLastError());
     const size_t smem = (size_t)p->nv * sizeof(float);
-    const dim3 grid((unsigned)p->n_cells);
+    const dim3 grid((unsigned)p->bp_blocks);
 #define LAUNCH(Z, PR)                                                                                         \
     do {                                                                                                      \
         if (smem > 40 * 1024)                                                                                 \
@@ -341,7 +371,7 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                                                              p->d_invw, p->d_w, scratch, vol, col_scale,      \
                                                              partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
                                                              p->lo[2], p->pitch[2], p->det00z, p->pv,         \
-                                                             p->flat_v, mode);                                \
+                                                             p->flat_v, mode, (int)p->nx, (int)p->ny);        \
     } while (0)
     switch (p->bp_zpt * 2 + (precise ? 1 : 0)) {
         case 2: LAUNCH(1, false); break;

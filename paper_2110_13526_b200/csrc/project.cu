@@ -200,16 +200,16 @@ __global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restr
     const int nst = (M + K - 1) / K;  // stages of K intervals
     const uint32_t col_bytes = (uint32_t)zs * 4u;
     if (producer) {
-        if (lane == 0) {
-            for (int i = 0; i < nst; ++i) {
-                const int slot = i % nstages, round = i / nstages;
-                if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
-                const int m0 = i * K, cnt = min(K, M - m0);
-                mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
-                float* dst = ring + (size_t)slot * K * zs;
-                for (int j = 0; j < cnt; ++j)
-                    bulk_g2s(dst + j * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + j].y), col_bytes, &full[slot]);
-            }
+        // one lane arms the stage's barrier, then lanes j < cnt each issue one bulk copy
+        for (int i = 0; i < nst; ++i) {
+            const int slot = i % nstages, round = i / nstages;
+            if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+            const int m0 = i * K, cnt = min(K, M - m0);
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
+            __syncwarp();
+            if (lane < cnt)
+                bulk_g2s(ring + ((size_t)slot * K + lane) * zs,
+                         vol + (uint32_t)__float_as_int(s_ent[m0 + lane].y), col_bytes, &full[slot]);
         }
     } else {
         float a = h.tau_start;
@@ -280,10 +280,13 @@ extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, d
         switch (p->proj_rpt * 10 + K) {
             case 12: LAUNCH_T(1, 2); break;
             case 14: LAUNCH_T(1, 4); break;
+            case 18: LAUNCH_T(1, 8); break;
             case 22: LAUNCH_T(2, 2); break;
             case 24: LAUNCH_T(2, 4); break;
+            case 28: LAUNCH_T(2, 8); break;
             case 42: LAUNCH_T(4, 2); break;
-            default: LAUNCH_T(4, 4); break;
+            case 44: LAUNCH_T(4, 4); break;
+            default: LAUNCH_T(4, 8); break;
         }
 #undef LAUNCH_T
         CBCT_CHECK(cudaGetLastError());
