@@ -212,7 +212,7 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
     if (lane == 0) pc[nv] = pc[nv + 1] = (float)carry;
 }
 
-template <int G, bool FLAT>
+template <int G, bool FLAT, bool TABLE>
 __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict__ cell_off,
                                                       const CellEntry* __restrict__ cell_ent,
                                                       const ColumnHeader* __restrict__ cols,
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                                                       double* __restrict__ partials, int nv, int nz, int zs,
                                                       double lo2, double p2, double det00z, double pv, int nx,
                                                       int ny) {
-    extern __shared__ float s_iw[];  // nv + 1 entries (s_iw[nv] = 0 pads the prefix end)
+    extern __shared__ float s_iw[];  // TABLE: nv + 1 entries of 1/rz (s_iw[nv] = 0)
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
     const int64_t cell = tiled_cell(blockIdx.x, nx, ny);
@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    for (int k = threadIdx.x; k <= nv; k += blockDim.x) s_iw[k] = k < nv ? invw[k] : 0.0f;
+    if (TABLE)
+        for (int k = threadIdx.x; k <= nv; k += blockDim.x) s_iw[k] = k < nv ? invw[k] : 0.0f;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     float z[G], acc[G], sgn[G];
@@ -253,6 +254,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     const double c0i = floor(c0d + 0.5);
     const float c0f = (float)(c0d - c0i);
     const int magic = 0x4B400000 - (int)c0i - 1;  // floor(W) + c0i + 1 via the 1.5*2^23 trick
+    const int c0ii = (int)c0i;
     const float wlo = (float)(-c0i - 1.0), whi = (float)((double)nv - c0i - 0.5);
     const float fpv = (float)pv;
     const float* __restrict__ pyb = pref;
@@ -280,7 +282,18 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                 W = fminf(fmaxf(W, wlo), whi);  // keeps floor(W) + c0i + 1 in [0, nv]
                 const int vh = __float_as_int(__fadd_rd(W, 12582912.0f)) - magic;
                 const float P0 = __ldg(pyc + vh), P1 = __ldg(pyc + vh + 1);
-                const float iw = s_iw[vh];
+                // 1/rz of the straddler: rz = pv ((vh - c0i) - c0f) is formed from an exact small
+                // integer, so its relative rounding stays ~1e-7 even near the mid-plane (rcp is
+                // cheaper for the LSU-bound loop than a bank-conflicted table lookup).
+                float iw;
+                if (TABLE) {
+                    iw = s_iw[vh];
+                } else {
+                    const float wv = fpv * ((float)(vh - c0ii) - c0f);
+                    float r;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(wv));  // 1 MUFU op, <= 1 ulp
+                    iw = vh < nv && wv != 0.0f ? r : 0.0f;
+                }
                 const float u = fmaf(z[g], iw, -t0.z);  // tau of z on the straddling ray
                 const bool neg = iw < 0.0f;
                 const float lo = neg ? fmaxf(u, t0.x) : t0.x;
@@ -329,15 +342,22 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v);
         CBCT_CHECK(cudaGetLastError());
-        const size_t smem = (size_t)(p->nv + 1) * sizeof(float);
+        const bool table = getenv("CBCT_BP_RCP") == nullptr;
+        const size_t smem = table ? (size_t)(p->nv + 1) * sizeof(float) : 0;
         const int64_t tiles = ((p->nx + 15) / 16) * ((p->ny + 15) / 16);
         const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \
         do {                                                                                                   \
-            if (smem > 16 * 1024)                                                                              \
-                CBCT_CHECK(cudaFuncSetAttribute(k_bp_boundary<G, FL>,                                          \
+            if (table) {                                                                                       \
+                CBCT_CHECK(cudaFuncSetAttribute(k_bp_boundary<G, FL, true>,                                    \
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
-            k_bp_boundary<G, FL><<<grid, p->bpg_threads, smem, s>>>(                                           \
+                k_bp_boundary<G, FL, true><<<grid, p->bpg_threads, smem, s>>>(                                 \
+                    p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,  \
+                    (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,  \
+                    (int)p->ny);                                                                               \
+                break;                                                                                         \
+            }                                                                                                  \
+            k_bp_boundary<G, FL, false><<<grid, p->bpg_threads, smem, s>>>(                                    \
                 p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
                 (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,      \
                 (int)p->ny);                                                                                   \
@@ -348,8 +368,14 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
             case 3: LAUNCH_G(1, true); break;
             case 4: LAUNCH_G(2, false); break;
             case 5: LAUNCH_G(2, true); break;
+            case 6: LAUNCH_G(3, false); break;
+            case 7: LAUNCH_G(3, true); break;
             case 8: LAUNCH_G(4, false); break;
-            default: LAUNCH_G(4, true); break;
+            case 9: LAUNCH_G(4, true); break;
+            case 10: LAUNCH_G(5, false); break;
+            case 11: LAUNCH_G(5, true); break;
+            case 12: LAUNCH_G(6, false); break;
+            default: LAUNCH_G(6, true); break;
         }
 #undef LAUNCH_G
         CBCT_CHECK(cudaGetLastError());

@@ -427,14 +427,39 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         const int64_t smem = 16 * ((2 * p->proj_tma_stages * 8 + 15) / 16) + (p->max_intervals + 4) * 8 +
                              (int64_t)p->proj_tma_stages * p->proj_tma_k * col_bytes;
         p->proj_tma = smem <= 200 * 1024 ? 1 : 0;
+        // prefix-sum projector: 2 ring stages + Qc of C cells, ~<= 64 KB
+        const int64_t per_c = 3 * col_bytes;
+        int cq = 32;
+        while (cq > 8 && per_c * cq + col_bytes > 64 * 1024) cq >>= 1;
+        if (const char* e = getenv("CBCT_PROJ_Q_C")) cq = atoi(e);
+        p->proj_q_c = cq;
+        const int64_t qsmem = 32 + (p->max_intervals + 3) * 8 + per_c * cq + col_bytes + (3 * cq + 1) * 4;
+        // the slab-parallel prefix pays off when rays outnumber z slabs (config 2: 1.45 rays/slab;
+        // config 3 has 0.92 and prefers the per-ray walk)
+        p->proj_q = (qsmem <= 220 * 1024 && (double)g->nv >= 1.2 * (double)zs) ? 1 : 0;
+        if (const char* e = getenv("CBCT_PROJ_Q")) p->proj_q = atoi(e);
     }
     p->bp_zpt = g->nz <= 512 ? 1 : (g->nz <= 1024 ? 2 : 4);
     p->bp_threads = (int)(((g->nz + p->bp_zpt - 1) / p->bp_zpt + 31) / 32 * 32);
     p->bp_blocks = (int32_t)(((g->nx + 15) / 16) * ((g->ny + 15) / 16) * 256);  // tiled grid (backproject.cu)
     {
-        const int64_t warps = (g->nz + 30) / 31;  // 31 voxels per warp (32 boundaries)
-        p->bpg_groups = warps <= 32 ? 1 : (warps <= 64 ? 2 : 4);
-        p->bpg_threads = (int)(((warps + p->bpg_groups - 1) / p->bpg_groups) * 32);
+        // 31 voxels per boundary group (32 boundaries = one warp's lanes); a warp runs G
+        // groups so the per-crossing shared loads are amortised (backproject.cu).  Pick
+        // G in [2, 6] covering the groups with the least waste, at most 32 warps.
+        const int64_t groups = (g->nz + 30) / 31;
+        int best_g = 1;
+        int64_t best_waste = INT64_MAX;
+        for (int G = 3; G <= 6; ++G) {
+            const int64_t warps = (groups + G - 1) / G;
+            if (warps > 32) continue;
+            const int64_t waste = warps * G - groups;
+            if (waste < best_waste) { best_waste = waste; best_g = G; }
+        }
+        if (best_waste == INT64_MAX) best_g = 6;
+        if (groups == 1) best_g = 1;
+        if (const char* e = getenv("CBCT_BP_G")) best_g = atoi(e);
+        p->bpg_groups = best_g;
+        p->bpg_threads = (int)(((groups + best_g - 1) / best_g) * 32);
     }
     p->table_bytes = total;
     cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);

@@ -257,12 +257,195 @@ __global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restr
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Column prefix-sum variant.  All rays of a detector column share the interval
+// sequence, so per chunk of C cells the CTA first builds, for every z slab,
+//     Qc[j][iz] = sum_{j' < j} dtau_j' * vol[cell_j', iz]          (phase 1, slab-parallel)
+// and each ray then adds  Qc[C][iz]  for the slab it leaves the chunk in, plus,
+// for every z-plane crossing inside the chunk, R_old(tz) - R_new(tz), where
+// R_iz(tau) interpolates Qc linearly inside the interval holding tau (phase 2).
+// This is the same segment sum as the interval walk, but the per-interval work is
+// done once per slab instead of once per ray, and the divergent per-ray work
+// only happens at z crossings.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int RPT, int C>
+__global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restrict__ cols,
+                                                   const int64_t* __restrict__ col_off,
+                                                   const float2* __restrict__ col_ent, const double* __restrict__ wtab,
+                                                   const float* __restrict__ vol, float* __restrict__ proj,
+                                                   double* __restrict__ partials, int nv, int nz, int zs, double lo2,
+                                                   double p2, int flat_v, int ent_cap) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
+    uint64_t* empty = full + 2;                               // [2]
+    float2* s_ent = reinterpret_cast<float2*>(smem_raw + 32);
+    float* ring = reinterpret_cast<float*>(s_ent + ent_cap);  // [2][C][zs]
+    float* qc = ring + 2 * C * zs;                             // [C+1][zs]
+    float* sB = qc + (C + 1) * zs;                             // [C+1] interval starts (+ chunk end)
+    float* sInv = sB + (C + 1);                                // [C]   1/dtau
+    float* sDl = sInv + C;                                     // [C]   dtau
+    const int nwc = (blockDim.x >> 5) - 1;
+    const int nct = nwc * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = warp == nwc;
+
+    const int64_t c = blockIdx.x;
+    const ColumnHeader h = cols[c];
+    const int64_t off = col_off[c];
+    const int M = (int)(col_off[c + 1] - off);
+    for (int k = threadIdx.x; k < M; k += blockDim.x) s_ent[k] = col_ent[off + k];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], nwc);
+        }
+        mbar_fence_init();
+    }
+    RayState st[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) ray_setup(st[r], h, producer ? nv : threadIdx.x + r * nct, nv, wtab, lo2, p2, nz, flat_v);
+    __syncthreads();
+
+    const int nch = (M + C - 1) / C;
+    const uint32_t col_bytes = (uint32_t)zs * 4u;
+    if (producer) {
+        for (int i = 0; i < nch; ++i) {
+            const int slot = i & 1, round = i >> 1;
+            if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+            const int m0 = i * C, cnt = min(C, M - m0);
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
+            __syncwarp();
+            if (lane < cnt)
+                bulk_g2s(ring + ((size_t)slot * C + lane) * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + lane].y),
+                         col_bytes, &full[slot]);
+        }
+    } else {
+        float chunk_start = h.tau_start;
+        for (int i = 0; i < nch; ++i) {
+            const int slot = i & 1, round = i >> 1;
+            const int m0 = i * C, cnt = min(C, M - m0);
+            // interval starts / inverse lengths of this chunk
+            for (int k = threadIdx.x; k <= cnt; k += nct) {
+                const float b = k == 0 ? chunk_start : s_ent[m0 + k - 1].x;
+                sB[k] = b;
+                if (k < cnt) {
+                    const float e = s_ent[m0 + k].x;
+                    sInv[k] = e > b ? 1.0f / (e - b) : 0.0f;  // fp32-degenerate interval
+                    sDl[k] = e - b;
+                }
+            }
+            mbar_wait(&full[slot], round & 1);
+            // phase 1: slab-parallel prefix over the chunk's intervals
+            named_bar(1, nct);  // sB / sDl visible
+            const float* stage = ring + (size_t)slot * C * zs;
+            for (int iz = threadIdx.x; iz < zs; iz += nct) {
+                const float* src = stage + iz;
+                float* dst = qc + iz;
+                float q = 0.0f;
+                dst[0] = 0.0f;
+                if (cnt == C) {
+#pragma unroll
+                    for (int j = 0; j < C; ++j) {
+                        q = fmaf(sDl[j], src[j * zs], q);
+                        dst[(j + 1) * zs] = q;
+                    }
+                } else {
+                    for (int j = 0; j < cnt; ++j) {
+                        q = fmaf(sDl[j], src[j * zs], q);
+                        dst[(j + 1) * zs] = q;
+                    }
+                }
+            }
+            named_bar(1, nct);
+            if (lane == 0) mbar_arrive(&empty[slot]);  // ring slot may be refilled
+            // phase 2: per ray, the slab it ends in plus one correction per z crossing
+            const float cend = sB[cnt];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                RayState& s = st[r];
+                while (s.tz < cend) {
+                    int m = 0;
+#pragma unroll
+                    for (int step = C / 2; step > 0; step >>= 1)
+                        if (m + step < cnt && sB[m + step] <= s.tz) m += step;
+                    const float f = (s.tz - sB[m]) * sInv[m];
+                    const float* q0 = qc + m * zs;
+                    const float* q1 = q0 + zs;
+                    const int izn = s.iz + s.dz;
+                    const float ro = fmaf(f, q1[s.iz] - q0[s.iz], q0[s.iz]);
+                    const float rn = fmaf(f, q1[izn] - q0[izn], q0[izn]);
+                    s.acc += ro - rn;
+                    s.iz = izn;
+                    s.jf += 1.0f;
+                    s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
+                }
+                s.acc += qc[cnt * zs + s.iz];
+            }
+            chunk_start = cend;
+            named_bar(1, nct);  // qc / sB reused by the next chunk
+        }
+    }
+
+    double sq = 0.0;
+    if (!producer) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            const int v = threadIdx.x + r * nct;
+            if (v < nv) {
+                const double w = wtab[v];
+                const float raylen = (float)sqrt(h.rxy2 + w * w);
+                const float out = st[r].acc * raylen;
+                proj[c * nv + v] = out;
+                sq += (double)out * (double)out;
+            }
+        }
+    }
+    if (partials) {
+        const double tot = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+    }
+}
+
 }  // namespace
 
 extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, double* partials, void* stream) {
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project: null argument");
     cudaStream_t s = (cudaStream_t)stream;
     const dim3 grid((unsigned)p->n_cols);
+    if (p->proj_q && getenv("CBCT_PROJ_LDG") == nullptr && getenv("CBCT_PROJ_TMA") == nullptr) {
+        const int Cq = p->proj_q_c;
+        const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
+        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)(2 * Cq + Cq + 1) * p->zs * 4 +
+                            (size_t)(3 * Cq + 1) * 4;
+        const int nt = p->proj_threads + 32;
+#define LAUNCH_Q(R, CC)                                                                                        \
+        do {                                                                                                   \
+            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                            (int)smem));                                                       \
+            k_project_q<R, CC><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj,  \
+                                                      partials, (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2],     \
+                                                      p->pitch[2], p->flat_v, ent_cap);                          \
+        } while (0)
+        switch (p->proj_rpt * 100 + Cq) {
+            case 108: LAUNCH_Q(1, 8); break;
+            case 116: LAUNCH_Q(1, 16); break;
+            case 132: LAUNCH_Q(1, 32); break;
+            case 208: LAUNCH_Q(2, 8); break;
+            case 216: LAUNCH_Q(2, 16); break;
+            case 232: LAUNCH_Q(2, 32); break;
+            case 408: LAUNCH_Q(4, 8); break;
+            case 416: LAUNCH_Q(4, 16); break;
+            default: LAUNCH_Q(4, 32); break;
+        }
+#undef LAUNCH_Q
+        CBCT_CHECK(cudaGetLastError());
+        cbct_count_launch();
+        return 0;
+    }
     if (p->proj_tma && getenv("CBCT_PROJ_LDG") == nullptr) {
         const int K = p->proj_tma_k, ns = p->proj_tma_stages;
         const int ent_cap = (int)((p->max_intervals + 2 + 1) / 2 * 2);
