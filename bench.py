@@ -269,7 +269,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / steps
-    value = world * 1e3 / ms_step  # replicas: every rank runs the whole iteration
+    value = 1e3 / ms_step
 
     # end-to-end through the public API: host fp64 b in, host x out, full solve
     b_host = op.proj_from_internal(b_int, torch.float64).cpu().numpy()
@@ -309,7 +309,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": "single",
                    "l2": "working set > 126 MB L2 (no flush needed)"},
         "gups_A": N ** 3 * V / (t_a * 1e-3) / 1e9, "gups_AT": N ** 3 * V / (t_at * 1e-3) / 1e9,
         "ms_A": t_a, "ms_AT": t_at, "ms_A_in_loop": t_a_loop, "ms_AT_in_loop": t_at_loop,
@@ -317,6 +317,115 @@ def run_ours(args, cfg, rank, world, local_rank):
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         "setup_s": t_setup, "plan_table_bytes": int(op.info.table_bytes),
         "e_last": run.rel(run.nb),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_sharded(args, cfg, rank, world, local_rank):
+    """N > 1: one CGLS solve sharded over the ranks (views for A, cell rows for A^T), NCCL all_gathers
+    of d and e per iteration (paper_2110_13526_b200/distributed.py).  Strong scaling: total work fixed."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200 import _lib
+    from paper_2110_13526_b200.distributed import CudaVectors, DistCglsRun, ShardedOperator, TorchComm
+    from paper_2110_13526_b200.solvers import SolverConfig
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    N, V, nu, nv, solver, K = CONFIGS[cfg]
+    vg, tr = geometry(cfg)
+    comm = TorchComm()
+    sop = ShardedOperator(vg, tr, comm, device=dev)
+    op = sop.op
+    truth = op.volume_to_internal(P.generate_phantom(P.shepp_logan_3d(), vg).data)
+    b_full = op.new_projections()
+    op.project_internal(truth, b_full)  # inverse crime b = A phantom; each rank keeps its view block
+    b_local = torch.zeros(sop.m_loc, device=dev)
+    blk = b_full[sop.v0 * sop.view_elems: sop.v1 * sop.view_elems]
+    b_local[: blk.numel()] = blk
+    del b_full, truth
+    vec = CudaVectors(op)
+    steps, warmup = args.steps, args.warmup
+    run = DistCglsRun(sop, vec, b_local, SolverConfig(method="cgls", max_iterations=steps + warmup + 1), record=False)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        run.step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().cbct_launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        start.record(stream)
+        for _ in range(steps):
+            run.step()
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.lib().cbct_launch_count() - launches0
+    t = torch.tensor([start.elapsed_time(end)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / steps
+
+    def kernel_ms(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(reps):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    t_a = kernel_ms(lambda: sop.project_local(sop._d_full, run.p))
+    t_at = kernel_ms(lambda: sop.backproject_local(sop._e_full, run.r))
+    tk = torch.tensor([t_a, t_at], device=dev)
+    dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+    t_a, t_at = (float(v) for v in tk.tolist())
+    # end to end: host view block in (pinned), sharded solve, x shards gathered to rank-0 host
+    e2e_k = max(steps, 5)
+    b_host = b_local.cpu().pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bl = b_host.to(dev, non_blocking=True)
+    r2 = DistCglsRun(sop, vec, bl, SolverConfig(method="cgls", max_iterations=e2e_k), record=False)
+    while r2.should_continue():
+        r2.step()
+    _, x_loc = r2.finish()
+    x_full = sop.gather_volume(x_loc)
+    x_host = x_full[: op.vol_elems].cpu() if rank == 0 else None
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    f_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    peak_slots = SMS * LANES * f_mhz * 1e6
+    nnz = NNZ[cfg]
+    nnz_a = nnz * (sop.v1 - sop.v0) / V  # views are symmetric: nnz splits evenly
+    dom, t_dom = ("A^T", t_at) if t_at >= t_a else ("A", t_a)
+    nnz_dom = nnz / world if dom == "A^T" else nnz_a
+    achieved = SLOTS_PER_NNZ * nnz_dom / (t_dom * 1e-3)
+    line = {
+        "metric": "CGLS iterations/sec", "value": 1e3 / ms_step, "unit": "it/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
+                   "parallelism": f"A by view x{world}, A^T by cell rows x{world}, NCCL all_gather d/e",
+                   "l2": "working set > 126 MB L2 (no flush needed)"},
+        "ms_A_local": t_a, "ms_AT_local": t_at,
+        "roofline": {"bound": "issue", "kernel": dom, "achieved": achieved / 1e9, "peak": peak_slots / 1e9,
+                     "unit": "Gslot/s", "frac": achieved / peak_slots, "traffic": None,
+                     "definition": "per-rank share of SURVEY.md 8(d) slots (A^T share approximated as nnz/N)"},
+        "cpu_baseline": None,
+        "e2e": {"value": e2e_k / float(te.item()), "unit": "it/s", "h2d_bytes_per_step": int(sop.m_loc * 4 / e2e_k),
+                "d2h_bytes_per_step": int(op.vol_elems * 4 / e2e_k) if rank == 0 else 0,
+                "note": f"sharded solve from pinned host view blocks, K={e2e_k}, incl. pre-loop and x gather"},
+        "clocks": clocks, "gpu_launches": int(launches),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -331,6 +440,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded (multi-GPU) driver even at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -338,10 +448,19 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, args.config, rank, world)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch
 
+        torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29531")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl")
+        rc = run_sharded(args, args.config, rank, world, local_rank)
+        torch.distributed.destroy_process_group()
+        return rc
     rc = run_ours(args, args.config, rank, world, local_rank)
     if world > 1:
         import torch

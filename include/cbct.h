@@ -112,6 +112,18 @@ int cbct_project(const cbct_plan* plan, const float* vol, float* proj, double* n
 int cbct_backproject(const cbct_plan* plan, const float* proj, float* vol, int mode, float* scratch_proj,
                      const float* col_scale, double* norm2_partials, void* stream);
 
+/* Sharded variants for the multi-GPU path.
+ * A restricted to views [view0, view1): proj receives the (view1-view0)*nu*nv values of that view
+ * block; norm2_partials (nullable) receives (view1-view0)*nu fp64 partials. */
+int cbct_project_views(const cbct_plan* plan, const float* vol, float* proj, int64_t view0, int64_t view1,
+                       double* norm2_partials, void* stream);
+/* A^T restricted to cell rows iy in [row0, row1): vol receives (row1-row0)*nx*zstride values (that
+ * slab of the device layout); col_scale is indexed like vol; norm2_partials receives
+ * ceil(nx/16)*ceil((row1-row0)/16)*256 fp64 partials.  proj is the full projection set. */
+int cbct_backproject_rows(const cbct_plan* plan, const float* proj, float* vol, int64_t row0, int64_t row1,
+                          int mode, float* scratch_proj, const float* col_scale, double* norm2_partials,
+                          void* stream);
+
 /* ---- layout conversion (reference layout <-> internal layout) ------------ */
 /* src: fp64 or fp32 (src_is_f64) reference-layout volume (nz,ny,nx) -> internal. */
 int cbct_volume_to_internal(const cbct_plan* plan, const void* src, int src_is_f64, float* dst, void* stream);

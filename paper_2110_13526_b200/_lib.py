@@ -53,6 +53,8 @@ SIGNATURES = {
     "cbct_plan_get_info": (c_i32, [c_p, ctypes.POINTER(PlanInfo)]),
     "cbct_project": (c_i32, [c_p, c_p, c_p, c_p, c_p]),
     "cbct_backproject": (c_i32, [c_p, c_p, c_p, c_i32, c_p, c_p, c_p, c_p]),
+    "cbct_project_views": (c_i32, [c_p, c_p, c_p, c_i64, c_i64, c_p, c_p]),
+    "cbct_backproject_rows": (c_i32, [c_p, c_p, c_p, c_i64, c_i64, c_i32, c_p, c_p, c_p, c_p]),
     "cbct_volume_to_internal": (c_i32, [c_p, c_p, c_i32, c_p, c_p]),
     "cbct_volume_from_internal": (c_i32, [c_p, c_p, c_p, c_i32, c_p]),
     "cbct_proj_to_internal": (c_i32, [c_p, c_p, c_i32, c_p, c_p]),

@@ -33,16 +33,16 @@ constexpr int kChunk = 256;
 
 // Cells are visited in 16x16 tiles so concurrently resident CTAs share the
 // detector columns they read (L2 locality of the prefix arrays).
-__device__ __forceinline__ int64_t tiled_cell(int64_t b, int nx, int ny) {
+// Rows [row0, row1) of cells only (a rank's slab in the sharded path).
+__device__ __forceinline__ int64_t tiled_cell(int64_t b, int nx, int row0, int row1) {
     const int T = 16;
     const int tx = (nx + T - 1) / T;
     const int64_t per_tile = (int64_t)T * T;
     const int64_t tile = b / per_tile;
     const int k = (int)(b - tile * per_tile);
-    const int ty0 = (int)(tile / tx) * T, tx0 = (int)(tile % tx) * T;
-    // cells of partial edge tiles are packed by skipping out-of-range slots in the host-computed grid
-    const int iy = ty0 + k / T, ix = tx0 + k % T;
-    if (ix >= nx || iy >= ny) return -1;
+    const int ty0 = row0 + (int)(tile / tx) * T, tx0 = (int)(tile % tx) * T;
+    const int iy = ty0 + k / T, ix = tx0 + k % T;  // padding slots of partial edge tiles return -1
+    if (ix >= nx || iy >= row1) return -1;
     return (int64_t)iy * nx + ix;
 }
 
@@ -68,10 +68,10 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
                                                      float* __restrict__ vol, const float* __restrict__ col_scale,
                                                      double* __restrict__ partials, int nv, int nz, int zs,
                                                      double lo2, double p2, double det00z, double pv, int flat_v,
-                                                     int mode, int nx, int ny) {
+                                                     int mode, int nx, int row0, int row1) {
     extern __shared__ float s_invw[];
     __shared__ Tri s_tri[kChunk];
-    const int64_t cell = tiled_cell(blockIdx.x, nx, ny);
+    const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
     if (cell < 0) {  // padding slot of an edge tile
         if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
         return;
@@ -144,13 +144,14 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
         }
     }
 
-    float* out = vol + cell * zs;
+    const int64_t lcell = cell - (int64_t)row0 * nx;  // local cell in the output slab
+    float* out = vol + lcell * zs;
     double sq = 0.0;
 #pragma unroll
     for (int r = 0; r < ZPT; ++r) {
         if (iz[r] < nz) {
             float val = acc[r];
-            if (col_scale) val *= col_scale[cell * zs + CBCT_ZPAD + iz[r]];
+            if (col_scale) val *= col_scale[lcell * zs + CBCT_ZPAD + iz[r]];
             out[CBCT_ZPAD + iz[r]] = val;
             sq += (double)val * (double)val;
         }
@@ -221,11 +222,11 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                                                       const float* __restrict__ col_scale,
                                                       double* __restrict__ partials, int nv, int nz, int zs,
                                                       double lo2, double p2, double det00z, double pv, int nx,
-                                                      int ny) {
+                                                      int row0, int row1) {
     extern __shared__ float s_iw[];  // TABLE: nv + 1 entries of 1/rz (s_iw[nv] = 0)
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
-    const int64_t cell = tiled_cell(blockIdx.x, nx, ny);
+    const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
     if (cell < 0) {  // padding slot of an edge tile
         if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
         return;
@@ -307,14 +308,15 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         }
     }
 
-    float* out = vol + cell * zs;
+    const int64_t lcell = cell - (int64_t)row0 * nx;  // local cell in the output slab
+    float* out = vol + lcell * zs;
     double sq = 0.0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int iz = kb[g];  // voxel [z_kb, z_kb+1)
         if (lane < 31 && iz < nz) {
             float val = acc[g];
-            if (col_scale) val *= col_scale[cell * zs + CBCT_ZPAD + iz];
+            if (col_scale) val *= col_scale[lcell * zs + CBCT_ZPAD + iz];
             out[CBCT_ZPAD + iz] = val;
             sq += (double)val * (double)val;
         }
@@ -328,8 +330,11 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
 
 }  // namespace
 
-extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vol, int mode, float* scratch,
-                                const float* col_scale, double* partials, void* stream) {
+extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, float* vol, int64_t row0, int64_t row1,
+                                     int mode, float* scratch, const float* col_scale, double* partials,
+                                     void* stream) {
+    if (p && (row0 < 0 || row1 > p->ny || row0 >= row1))
+        return cbct_fail(CBCT_E_ARG, "cbct_backproject: bad row range");
     if (!p || !vol || !scratch) return cbct_fail(CBCT_E_ARG, "cbct_backproject: null argument");
     if (mode != 1 && mode != 2) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode must be 1 or 2");
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode 1 needs projections");
@@ -344,7 +349,7 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
         CBCT_CHECK(cudaGetLastError());
         const bool table = getenv("CBCT_BP_RCP") == nullptr;
         const size_t smem = table ? (size_t)(p->nv + 1) * sizeof(float) : 0;
-        const int64_t tiles = ((p->nx + 15) / 16) * ((p->ny + 15) / 16);
+        const int64_t tiles = ((p->nx + 15) / 16) * ((row1 - row0 + 15) / 16);
         const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \
         do {                                                                                                   \
@@ -354,13 +359,13 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                 k_bp_boundary<G, FL, true><<<grid, p->bpg_threads, smem, s>>>(                                 \
                     p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,  \
                     (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,  \
-                    (int)p->ny);                                                                               \
+                    (int)row0, (int)row1);                                                                               \
                 break;                                                                                         \
             }                                                                                                  \
             k_bp_boundary<G, FL, false><<<grid, p->bpg_threads, smem, s>>>(                                    \
                 p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
                 (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,      \
-                (int)p->ny);                                                                                   \
+                (int)row0, (int)row1);                                                                                   \
         } while (0)
         const bool fl = p->flat_v >= 0;
         switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
@@ -387,7 +392,7 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                                                                  scratch, p->n_cols, (int)p->nv);
     CBCT_CHECK(cudaGetLastError());
     const size_t smem = (size_t)p->nv * sizeof(float);
-    const dim3 grid((unsigned)p->bp_blocks);
+    const dim3 grid((unsigned)(((p->nx + 15) / 16) * ((row1 - row0 + 15) / 16) * 256));
 #define LAUNCH(Z, PR)                                                                                         \
     do {                                                                                                      \
         if (smem > 40 * 1024)                                                                                 \
@@ -397,7 +402,7 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
                                                              p->d_invw, p->d_w, scratch, vol, col_scale,      \
                                                              partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
                                                              p->lo[2], p->pitch[2], p->det00z, p->pv,         \
-                                                             p->flat_v, mode, (int)p->nx, (int)p->ny);        \
+                                                             p->flat_v, mode, (int)p->nx, (int)row0, (int)row1);        \
     } while (0)
     switch (p->bp_zpt * 2 + (precise ? 1 : 0)) {
         case 2: LAUNCH(1, false); break;
@@ -411,4 +416,10 @@ extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vo
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch(2);
     return 0;
+}
+
+extern "C" int cbct_backproject(const cbct_plan* p, const float* proj, float* vol, int mode, float* scratch,
+                                const float* col_scale, double* partials, void* stream) {
+    if (!p) return cbct_fail(CBCT_E_ARG, "cbct_backproject: null plan");
+    return cbct_backproject_rows(p, proj, vol, 0, p->ny, mode, scratch, col_scale, partials, stream);
 }

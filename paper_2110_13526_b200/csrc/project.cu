@@ -91,10 +91,10 @@ __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict_
                                                  const float2* __restrict__ col_ent, const double* __restrict__ wtab,
                                                  const float* __restrict__ vol, float* __restrict__ proj,
                                                  double* __restrict__ partials, int nv, int nz, double lo2,
-                                                 double p2, int flat_v) {
+                                                 double p2, int flat_v, int64_t c0) {
     extern __shared__ float4 s_ent4[];  // column entries, two per float4, padded to an even count
     float2* s_ent = reinterpret_cast<float2*>(s_ent4);
-    const int64_t c = blockIdx.x;
+    const int64_t c = c0 + blockIdx.x;  // detector column (view * nu + u)
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(512) k_project(const ColumnHeader* __restrict_
             const double w = wtab[v];
             const float raylen = (float)sqrt(h.rxy2 + w * w);  // operator.py:102
             const float out = st[r].acc * raylen;
-            proj[c * nv + v] = out;
+            proj[(c - c0) * nv + v] = out;
             sq += (double)out * (double)out;
         }
     }
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restr
                                                      const double* __restrict__ wtab, const float* __restrict__ vol,
                                                      float* __restrict__ proj, double* __restrict__ partials, int nv,
                                                      int nz, int zs, double lo2, double p2, int flat_v, int nstages,
-                                                     int ent_cap) {
+                                                     int ent_cap, int64_t c0) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t* empty = full + nstages;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = warp == nwc;
 
-    const int64_t c = blockIdx.x;
+    const int64_t c = c0 + blockIdx.x;  // detector column (view * nu + u)
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(544) k_project_tma(const ColumnHeader* __restr
                 const double w = wtab[v];
                 const float raylen = (float)sqrt(h.rxy2 + w * w);
                 const float out = st[r].acc * raylen;
-                proj[c * nv + v] = out;
+                proj[(c - c0) * nv + v] = out;
                 sq += (double)out * (double)out;
             }
         }
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                                                    const float2* __restrict__ col_ent, const double* __restrict__ wtab,
                                                    const float* __restrict__ vol, float* __restrict__ proj,
                                                    double* __restrict__ partials, int nv, int nz, int zs, double lo2,
-                                                   double p2, int flat_v, int ent_cap) {
+                                                   double p2, int flat_v, int ent_cap, int64_t c0) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
     uint64_t* empty = full + 2;                               // [2]
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = warp == nwc;
 
-    const int64_t c = blockIdx.x;
+    const int64_t c = c0 + blockIdx.x;  // detector column (view * nu + u)
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                 const double w = wtab[v];
                 const float raylen = (float)sqrt(h.rxy2 + w * w);
                 const float out = st[r].acc * raylen;
-                proj[c * nv + v] = out;
+                proj[(c - c0) * nv + v] = out;
                 sq += (double)out * (double)out;
             }
         }
@@ -412,10 +412,13 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
 
 }  // namespace
 
-extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, double* partials, void* stream) {
+extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* proj, int64_t view0, int64_t view1,
+                                  double* partials, void* stream) {
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project: null argument");
+    if (view0 < 0 || view1 > p->V || view0 >= view1) return cbct_fail(CBCT_E_ARG, "cbct_project: bad view range");
     cudaStream_t s = (cudaStream_t)stream;
-    const dim3 grid((unsigned)p->n_cols);
+    const int64_t c0 = view0 * p->nu;
+    const dim3 grid((unsigned)((view1 - view0) * p->nu));
     if (p->proj_q && getenv("CBCT_PROJ_LDG") == nullptr && getenv("CBCT_PROJ_TMA") == nullptr) {
         const int Cq = p->proj_q_c;
         const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
@@ -428,7 +431,7 @@ extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, d
                                             (int)smem));                                                       \
             k_project_q<R, CC><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj,  \
                                                       partials, (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2],     \
-                                                      p->pitch[2], p->flat_v, ent_cap);                          \
+                                                      p->pitch[2], p->flat_v, ent_cap, c0);                      \
         } while (0)
         switch (p->proj_rpt * 100 + Cq) {
             case 108: LAUNCH_Q(1, 8); break;
@@ -458,7 +461,7 @@ extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, d
                                             (int)smem));                                                       \
             k_project_tma<R, KK><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol,      \
                                                         proj, partials, (int)p->nv, (int)p->nz, (int)p->zs,      \
-                                                        p->lo[2], p->pitch[2], p->flat_v, ns, ent_cap);          \
+                                                        p->lo[2], p->pitch[2], p->flat_v, ns, ent_cap, c0);      \
         } while (0)
         switch (p->proj_rpt * 10 + K) {
             case 12: LAUNCH_T(1, 2); break;
@@ -484,7 +487,7 @@ extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, d
             CBCT_CHECK(cudaFuncSetAttribute(k_project<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                             (int)smem));                                                     \
         k_project<R><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj,        \
-                                            partials, (int)p->nv, (int)p->nz, p->lo[2], p->pitch[2], p->flat_v); \
+                                            partials, (int)p->nv, (int)p->nz, p->lo[2], p->pitch[2], p->flat_v, c0); \
     } while (0)
     switch (p->proj_rpt) {
         case 1: LAUNCH(1); break;
@@ -495,4 +498,9 @@ extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, d
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();
     return 0;
+}
+
+extern "C" int cbct_project(const cbct_plan* p, const float* vol, float* proj, double* partials, void* stream) {
+    if (!p) return cbct_fail(CBCT_E_ARG, "cbct_project: null plan");
+    return cbct_project_views(p, vol, proj, 0, p->V, partials, stream);
 }

@@ -1,0 +1,249 @@
+"""Multi-GPU CGLS: projection space sharded by view, volume space by cell rows.
+
+One process per GPU (torchrun), NCCL over NVLink for the exchanges (SURVEY.md 8(e),
+DESIGN.md section 5):
+
+* rank r owns the view block [v0, v1) of every projection-space vector (b, e, p) --
+  contiguous in the [V][nu][nv] device layout -- and applies A to those views;
+* rank r owns the cell rows [y0, y1) of every volume-space vector (x, d, r) --
+  contiguous in the [ny][nx][zs] device layout -- and applies A^T to those cells
+  (gathering over all views);
+* per CGLS iteration: all_gather(d) before A, all_gather(e) before A^T, and the
+  three squared norms as per-rank fp64 partials gathered and summed in rank order
+  (bitwise reproducible for a fixed world size).
+
+Shards are equal-sized (the last one zero-padded), so the gathered buffer *is* the
+full device layout and the CUDA kernels read it unchanged.  The driver is written
+against two small interfaces -- a local operator (project_local / backproject_local)
+and a vector backend -- so the same recurrences are exercised on CPU with gloo in
+tests/test_distributed_cpu.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+
+import numpy as np
+import torch
+
+from ._lib import call
+from .solvers import ConvergenceRecord, SolverReport, SolverConfig
+
+__all__ = ["block", "ShardedOperator", "CudaVectors", "TorchComm", "DistCglsRun", "dist_cgls", "gathered_report"]
+
+
+def block(n: int, world: int, rank: int):
+    """Equal-size contiguous block of n items for `rank`: (lo, hi, per); hi - lo may be < per."""
+    per = -(-n // world)
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per), per
+
+
+class TorchComm:
+    """torch.distributed collectives used by the driver (NCCL on GPU, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, local: torch.Tensor, full: torch.Tensor) -> torch.Tensor:
+        self.dist.all_gather_into_tensor(full, local, group=self.group)
+        return full
+
+    def allsum(self, value: float, device) -> float:
+        """Sum of per-rank fp64 partials in rank order (deterministic for a fixed world)."""
+        t = torch.tensor([value], dtype=torch.float64, device=device)
+        out = torch.empty(self.world, dtype=torch.float64, device=device)
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        acc = 0.0
+        for v in out.cpu().tolist():
+            acc += v
+        return acc
+
+
+class CudaVectors:
+    """Vector backend on libcbct's fused kernels (deterministic fp64 partials)."""
+
+    def __init__(self, op):
+        from .solvers import _Dev
+
+        self.dev = _Dev(op)
+
+    def axpby(self, a, x, b, y, norm2=False):
+        return self.dev.axpby(a, x, b, y, norm2=norm2)
+
+    def sub(self, a, b, out, norm2=False):
+        return self.dev.sub(a, b, out, norm2=norm2)
+
+    def update2(self, x, d, r, a_prev, do_x, beta):
+        self.dev.update2(x, d, r, a_prev, do_x, beta)
+
+    def sumsq(self, y):
+        return self.dev.sumsq(y)
+
+
+class ShardedOperator:
+    """Rank-local A (own views, full volume in) and A^T (own cell rows, all views in) on one GPU."""
+
+    def __init__(self, vol_geom, trajectory, comm, device=None):
+        from .operator import CbctOperator
+
+        self.comm = comm
+        self.world, self.rank = comm.world, comm.rank
+        self.op = CbctOperator(vol_geom, trajectory, device=device)
+        self.device = self.op.device
+        det = trajectory.detector
+        self.v0, self.v1, vper = block(trajectory.n_views, self.world, self.rank)
+        self.y0, self.y1, yper = block(vol_geom.ny, self.world, self.rank)
+        self.view_elems = det.nu * det.nv
+        self.row_elems = vol_geom.nx * self.op.zstride
+        self.m_loc = vper * self.view_elems
+        self.n_loc = yper * self.row_elems
+        self.m_full = self.world * self.m_loc
+        self.n_full = self.world * self.n_loc
+        self.nu = det.nu
+        self.nx = vol_geom.nx
+        nparts = max(vper * det.nu, -(-vol_geom.nx // 16) * -(-yper // 16) * 256, 1)
+        self._parts = torch.empty(nparts, dtype=torch.float64, device=self.device)
+        self._scratch = self.op.new_bp_scratch()
+        self._d_full = torch.zeros(self.n_full, dtype=torch.float32, device=self.device)
+        self._e_full = torch.zeros(self.m_full, dtype=torch.float32, device=self.device)
+
+    def _s(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _p(self, t):
+        return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    def _reduce(self, n):
+        call("cbct_reduce_partials", self._p(self._parts), int(n), self._p(self.op._red),
+             ctypes.byref(self.op._host), self._s())
+        return float(self.op._host.value)
+
+    def gather_volume(self, local):
+        return self.comm.all_gather(local, self._d_full)
+
+    def gather_proj(self, local):
+        return self.comm.all_gather(local, self._e_full)
+
+    def project_local(self, d_full, p_local, norm2=False):
+        """p_local = (A d)[views v0..v1) ; returns the local ||p||^2 partial."""
+        if self.v1 <= self.v0:
+            return 0.0 if norm2 else None
+        n = (self.v1 - self.v0) * self.nu
+        call("cbct_project_views", self.op._plan, self._p(d_full), self._p(p_local), self.v0, self.v1,
+             self._p(self._parts) if norm2 else None, self._s())
+        return self._reduce(n) if norm2 else None
+
+    def backproject_local(self, e_full, r_local, norm2=False):
+        """r_local = (A^T e)[cell rows y0..y1) ; returns the local ||r||^2 partial."""
+        if self.y1 <= self.y0:
+            return 0.0 if norm2 else None
+        n = -(-self.nx // 16) * -(-(self.y1 - self.y0) // 16) * 256
+        call("cbct_backproject_rows", self.op._plan, self._p(e_full), self._p(r_local), self.y0, self.y1, 1,
+             self._p(self._scratch), None, self._p(self._parts) if norm2 else None, self._s())
+        return self._reduce(n) if norm2 else None
+
+
+class DistCglsRun:
+    """Sharded CGLS state (solvers.py:269-358 recurrences).  ``__init__`` runs the pre-loop
+    (2 A + 1 A^T, first update folded in); ``step`` one loop iteration (1 A^T + 1 A, one
+    all_gather each, two fused vector passes, three rank-ordered scalar reductions)."""
+
+    def __init__(self, sop, vec, b_local: torch.Tensor, cfg: SolverConfig, record: bool = True, x0_local=None):
+        self.sop, self.vec, self.cfg, self.record = sop, vec, cfg, record
+        comm = sop.comm
+        dev = b_local.device
+        self.allsum = lambda v: comm.allsum(v, dev)  # noqa: E731
+        self.t0 = time.perf_counter()
+        self.b = b_local
+        self.x = torch.zeros(sop.n_loc, dtype=b_local.dtype, device=dev) if x0_local is None else x0_local.clone()
+        self.d = torch.zeros_like(self.x)
+        self.r = torch.zeros_like(self.x)
+        self.e = torch.zeros_like(b_local)
+        self.p = torch.zeros_like(b_local)
+        self.nb0 = math.sqrt(self.allsum(vec.sumsq(b_local)))
+        self.hist = []
+        self.i = 0
+        self.pending = 0.0
+        self.done = self.breakdown = False
+        sop.project_local(sop.gather_volume(self.x), self.p)
+        vec.sub(b_local, self.p, self.e)
+        self.nr2_old = self.allsum(sop.backproject_local(sop.gather_proj(self.e), self.r, norm2=True))
+        self.nb = math.sqrt(self.allsum(vec.sumsq(self.e)))
+        if self.nr2_old == 0.0:
+            self._rec(0)
+            self.done = self.breakdown = True
+            return
+        self.d.copy_(self.r)
+        np2 = self.allsum(sop.project_local(sop.gather_volume(self.d), self.p, norm2=True))
+        if np2 == 0.0:
+            self._rec(0)
+            self.done = self.breakdown = True
+            return
+        self.pending = self.nr2_old / np2
+        self.nb = math.sqrt(self.allsum(vec.axpby(-self.pending, self.p, 1.0, self.e, norm2=True)))
+        self._rec(0)
+
+    def rel(self, v):
+        return v / self.nb0 if self.nb0 > 0 else 0.0
+
+    def _rec(self, i):
+        if self.record:
+            self.hist.append(ConvergenceRecord(i, time.perf_counter() - self.t0, self.rel(self.nb), None))
+
+    def should_continue(self):
+        return not self.done and self.rel(self.nb) > self.cfg.rel_discrepancy_tol and \
+            self.i < self.cfg.max_iterations
+
+    def step(self) -> bool:
+        sop, vec = self.sop, self.vec
+        nr2 = self.allsum(sop.backproject_local(sop.gather_proj(self.e), self.r, norm2=True))
+        if nr2 == 0.0:
+            self.done = self.breakdown = True
+            return False
+        beta = nr2 / self.nr2_old
+        vec.update2(self.x, self.d, self.r, self.pending, self.pending != 0.0, beta)
+        self.pending = 0.0
+        self.nr2_old = nr2
+        np2 = self.allsum(sop.project_local(sop.gather_volume(self.d), self.p, norm2=True))
+        if np2 == 0.0:
+            self.done = self.breakdown = True
+            return False
+        self.pending = self.nr2_old / np2
+        self.nb = math.sqrt(self.allsum(vec.axpby(-self.pending, self.p, 1.0, self.e, norm2=True)))
+        self.i += 1
+        self._rec(self.i)
+        return True
+
+    def finish(self):
+        if self.pending != 0.0:
+            self.vec.axpby(self.pending, self.d, 1.0, self.x)
+            self.pending = 0.0
+        return {"iterations": self.i, "final_discrepancy_norm": self.nb, "history": self.hist,
+                "breakdown": self.breakdown, "worker_count": self.sop.comm.world}, self.x
+
+
+def dist_cgls(sop, vec, b_local: torch.Tensor, cfg: SolverConfig, record: bool = True, x0_local=None):
+    """Run sharded CGLS to completion; returns (info dict, local x shard)."""
+    run = DistCglsRun(sop, vec, b_local, cfg, record, x0_local)
+    while run.should_continue():
+        if not run.step():
+            break
+    return run.finish()
+
+
+def gathered_report(sop, x_local, info) -> SolverReport:
+    """Gather the volume shards and report like the single-GPU solvers (reference layout)."""
+    from .phantom import Volume
+
+    full = sop.gather_volume(x_local)[: sop.op.vol_elems]
+    xr = sop.op.volume_from_internal(full, torch.float64).cpu().numpy()
+    return SolverReport(Volume(sop.op.vol_geom, xr), info["iterations"], info["final_discrepancy_norm"],
+                        info["history"], info["worker_count"], info["breakdown"])
