@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                                                       double* __restrict__ partials, int nv, int nz, int zs,
                                                       double lo2, double p2, double det00z, double pv, int nx,
                                                       int row0, int row1) {
-    extern __shared__ float s_iw[];  // TABLE: nv + 1 entries of 1/rz (s_iw[nv] = 0)
+    extern __shared__ float s_iw[];  // 2 x (nv + 1): 1/rz (pad 0); 1/rz for rz < 0, else -inf
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
     const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
@@ -233,11 +233,15 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    if (TABLE)
-        for (int k = threadIdx.x; k <= nv; k += blockDim.x) s_iw[k] = k < nv ? invw[k] : 0.0f;
+    float* s_iwn = s_iw + (nv + 1);
+    for (int k = threadIdx.x; k <= nv; k += blockDim.x) {
+        const float iw = k < nv ? invw[k] : 0.0f;
+        s_iw[k] = iw;
+        s_iwn[k] = (k < nv && iw < 0.0f) ? iw : -INFINITY;
+    }
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    float z[G], acc[G], sgn[G];
+    float z[G], acc[G], sgn[G], sgn2[G];
     int kb[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -245,7 +249,10 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         z[g] = (float)(lo2 + (double)kb[g] * p2);
         acc[g] = 0.0f;
         sgn[g] = z[g] >= 0.0f ? 1.0f : 0.0f;
+        sgn2[g] = z[g] >= 0.0f ? 1.0f : -1.0f;
     }
+    const float* tbl[G];
+    float wbnd[G];
     // Row coordinate of a ray through height z at parameter t: v = z/(t pv) + c0,
     // c0 = -det00z/pv (= nv/2 - 1/2 without a principal-point offset).  c0 is split
     // into an integer and a fraction so the fp32 FFMA only carries z/(t pv) + frac:
@@ -259,6 +266,11 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     const float wlo = (float)(-c0i - 1.0), whi = (float)((double)nv - c0i - 0.5);
     const float fpv = (float)pv;
     const float* __restrict__ pyb = pref;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        tbl[g] = sgn[g] != 0.0f ? s_iw : s_iwn;
+        wbnd[g] = sgn[g] != 0.0f ? whi : wlo;
+    }
 
     for (int base = 0; base < ne; base += kChunk) {
         const int nch = min(kChunk, ne - base);
@@ -267,43 +279,41 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
             const CellEntry ce = cell_ent[off + base + k];
             const ColumnHeader& h = cols[ce.vu];
             const float ta = ce.tau_a, tb = ce.tau_b, tr = h.t_ref;
-            s_t0[k] = make_float4(ta, tb, tr, tb - ta);
-            s_t1[k] = make_float4(1.0f / ((ta + tr) * fpv), 1.0f / ((tb + tr) * fpv), FLAT ? flatw[ce.vu] : 0.0f, 0.0f);
+            const float dt = tb - ta;
+            const float idt = dt > 0.0f ? 1.0f / dt : 0.0f;
+            // {1/(t_a pv), 1/(t_b pv), t_ref, dt}, {1/dt, -t_a/dt, t_b/dt, flat-row weight}
+            const float ia = 1.0f / ((ta + tr) * fpv), ib = 1.0f / ((tb + tr) * fpv);
+            // side-blended forms: value = below + up01 * (above - below), up01 in {0, 1} per lane
+            s_t0[k] = make_float4(ia, ib - ia, tr, dt);
+            s_t1[k] = make_float4(idt, tb * idt, -(ta + tb) * idt, FLAT ? flatw[ce.vu] : 0.0f);
             s_vu[k] = ce.vu;
             s_fs[k] = FLAT ? h.flat_slab : 0;
         }
         __syncthreads();
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float* __restrict__ pyc = pyb + (int64_t)s_vu[k] * (nv + 2);
+            const float* pyc = pyb + (size_t)(uint32_t)s_vu[k] * (uint32_t)(nv + 2);
+            asm("mov.b64 %0, %0;" : "+l"(pyc));  // keep the column base in a register (1 IMAD.WIDE per lookup)
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const float ip = sgn[g] != 0.0f ? t1.y : t1.x;  // t* = t_b above the mid-plane, t_a below
-                float W = fmaf(z[g], ip, c0f);
-                W = fminf(fmaxf(W, wlo), whi);  // keeps floor(W) + c0i + 1 in [0, nv]
-                const int vh = __float_as_int(__fadd_rd(W, 12582912.0f)) - magic;
+                // V(z): rays entirely below z, with t* = t_b above the mid-plane and t_a below
+                // (blended with the lane's up01 so no select sits on the ALU pipe).
+                float W = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
+                W = sgn[g] != 0.0f ? fminf(W, wbnd[g]) : fmaxf(W, wbnd[g]);  // other side cannot overflow
+                const uint32_t vh = (uint32_t)(__float_as_int(__fadd_rd(W, 12582912.0f)) - magic);
                 const float P0 = __ldg(pyc + vh), P1 = __ldg(pyc + vh + 1);
-                // 1/rz of the straddler: rz = pv ((vh - c0i) - c0f) is formed from an exact small
-                // integer, so its relative rounding stays ~1e-7 even near the mid-plane (rcp is
-                // cheaper for the LSU-bound loop than a bank-conflicted table lookup).
-                float iw;
-                if (TABLE) {
-                    iw = s_iw[vh];
-                } else {
-                    const float wv = fpv * ((float)(vh - c0ii) - c0f);
-                    float r;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(wv));  // 1 MUFU op, <= 1 ulp
-                    iw = vh < nv && wv != 0.0f ? r : 0.0f;
-                }
-                const float u = fmaf(z[g], iw, -t0.z);  // tau of z on the straddling ray
-                const bool neg = iw < 0.0f;
-                const float lo = neg ? fmaxf(u, t0.x) : t0.x;
-                const float hi = neg ? t0.y : fminf(u, t0.y);
-                const float F = fmaxf(hi - lo, 0.0f);
-                float Gv = fmaf(F, P1 - P0, t0.w * P0);
+                // Straddler (ray vh): fraction of [t_a, t_b] below z as one saturated FFMA
+                // (FMA pipe); below the mid-plane the table holds -inf for rz >= 0 rays, which
+                // saturates to 0 (such a ray cannot straddle a negative z).
+                const float iw = tbl[g][vh];
+                const float u = fmaf(z[g], iw, -t0.z);
+                // above: (u - t_a)/dt = u/dt - t_a/dt ; below: (t_b - u)/dt   (t_a/dt = t_b/dt - 1)
+                const float kap = fmaf(sgn[g], t1.z, t1.y);  // up: -t_a/dt, down: t_b/dt
+                const float f = __saturatef(fmaf(u, sgn2[g] * t1.x, kap));
+                const float Gv = t0.w * fmaf(f, P1 - P0, P0);
                 const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
                 acc[g] += Gn - Gv;
-                if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.z : 0.0f;
+                if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.w : 0.0f;
             }
         }
     }
@@ -347,8 +357,8 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v);
         CBCT_CHECK(cudaGetLastError());
-        const bool table = getenv("CBCT_BP_RCP") == nullptr;
-        const size_t smem = table ? (size_t)(p->nv + 1) * sizeof(float) : 0;
+        const bool table = true;  // the 1/rz tables beat rcp.approx (measured)
+        const size_t smem = 2 * (size_t)(p->nv + 1) * sizeof(float);
         const int64_t tiles = ((p->nx + 15) / 16) * ((row1 - row0 + 15) / 16);
         const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \
