@@ -428,15 +428,15 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
                              (int64_t)p->proj_tma_stages * p->proj_tma_k * col_bytes;
         p->proj_tma = smem <= 200 * 1024 ? 1 : 0;
         // prefix-sum projector: 2 ring stages + Qc of C cells, ~<= 64 KB
-        const int64_t per_c = 3 * col_bytes;
-        int cq = 32;
-        while (cq > 8 && per_c * cq + col_bytes > 64 * 1024) cq >>= 1;
+        const int64_t per_c = 2 * col_bytes;  // two ring slots; the prefix is built in place
+        int cq = 16;
+        while (cq > 8 && per_c * cq > 72 * 1024) cq >>= 1;
         if (const char* e = getenv("CBCT_PROJ_Q_C")) cq = atoi(e);
         p->proj_q_c = cq;
-        const int64_t qsmem = 32 + (p->max_intervals + 3) * 8 + per_c * cq + col_bytes + (3 * cq + 1) * 4;
-        // the slab-parallel prefix pays off when rays outnumber z slabs (config 2: 1.45 rays/slab;
-        // config 3 has 0.92 and prefers the per-ray walk)
-        p->proj_q = (qsmem <= 220 * 1024 && (double)g->nv >= 1.2 * (double)zs) ? 1 : 0;
+        const int64_t qsmem = 32 + (p->max_intervals + 3) * 8 + per_c * cq + (3 * cq + 1) * 4;
+        // the slab-parallel prefix pays off unless z slabs far outnumber rays (measured: config 1
+        // 0.11 vs 0.22 ms, config 2 11.0 vs 15.0 ms, config 3 86 vs 115 ms against the TMA walk)
+        p->proj_q = (qsmem <= 220 * 1024 && (double)g->nv >= 0.5 * (double)zs) ? 1 : 0;
         if (const char* e = getenv("CBCT_PROJ_Q")) p->proj_q = atoi(e);
     }
     p->bp_zpt = g->nz <= 512 ? 1 : (g->nz <= 1024 ? 2 : 4);

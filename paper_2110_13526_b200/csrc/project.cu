@@ -283,9 +283,8 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
     uint64_t* empty = full + 2;                               // [2]
     float2* s_ent = reinterpret_cast<float2*>(smem_raw + 32);
-    float* ring = reinterpret_cast<float*>(s_ent + ent_cap);  // [2][C][zs]
-    float* qc = ring + 2 * C * zs;                             // [C+1][zs]
-    float* sB = qc + (C + 1) * zs;                             // [C+1] interval starts (+ chunk end)
+    float* ring = reinterpret_cast<float*>(s_ent + ent_cap);  // [2][C][zs]: staged columns, then Qc in place
+    float* sB = ring + 2 * C * zs;                             // [C+1] interval starts (+ chunk end)
     float* sInv = sB + (C + 1);                                // [C]   1/dtau
     float* sDl = sInv + C;                                     // [C]   dtau
     const int nwc = (blockDim.x >> 5) - 1;
@@ -308,6 +307,8 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     RayState st[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) ray_setup(st[r], h, producer ? nv : threadIdx.x + r * nct, nv, wtab, lo2, p2, nz, flat_v);
+    const float wlo = (float)fmin(wtab[0], wtab[nv - 1]), whi = (float)fmax(wtab[0], wtab[nv - 1]);
+    const float tref = h.t_ref, lo2f = (float)lo2, ip2 = (float)(1.0 / p2);
     __syncthreads();
 
     const int nch = (M + C - 1) / C;
@@ -315,12 +316,12 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     if (producer) {
         for (int i = 0; i < nch; ++i) {
             const int slot = i & 1, round = i >> 1;
-            if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+            if (round > 0) mbar_wait_backoff(&empty[slot], (round - 1) & 1);
             const int m0 = i * C, cnt = min(C, M - m0);
             if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
             __syncwarp();
-            if (lane < cnt)
-                bulk_g2s(ring + ((size_t)slot * C + lane) * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + lane].y),
+            for (int j = lane; j < cnt; j += 32)
+                bulk_g2s(ring + ((size_t)slot * C + j) * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + j].y),
                          col_bytes, &full[slot]);
         }
     } else {
@@ -328,42 +329,49 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
         for (int i = 0; i < nch; ++i) {
             const int slot = i & 1, round = i >> 1;
             const int m0 = i * C, cnt = min(C, M - m0);
-            // interval starts / inverse lengths of this chunk
             for (int k = threadIdx.x; k <= cnt; k += nct) {
-                const float b = k == 0 ? chunk_start : s_ent[m0 + k - 1].x;
-                sB[k] = b;
+                const float bb = k == 0 ? chunk_start : s_ent[m0 + k - 1].x;
+                sB[k] = bb;
                 if (k < cnt) {
                     const float e = s_ent[m0 + k].x;
-                    sInv[k] = e > b ? 1.0f / (e - b) : 0.0f;  // fp32-degenerate interval
-                    sDl[k] = e - b;
+                    sInv[k] = e > bb ? 1.0f / (e - bb) : 0.0f;  // fp32-degenerate interval
+                    sDl[k] = e - bb;
                 }
             }
             mbar_wait(&full[slot], round & 1);
-            // phase 1: slab-parallel prefix over the chunk's intervals
             named_bar(1, nct);  // sB / sDl visible
-            const float* stage = ring + (size_t)slot * C * zs;
-            for (int iz = threadIdx.x; iz < zs; iz += nct) {
-                const float* src = stage + iz;
-                float* dst = qc + iz;
-                float q = 0.0f;
-                dst[0] = 0.0f;
-                if (cnt == C) {
-#pragma unroll
-                    for (int j = 0; j < C; ++j) {
-                        q = fmaf(sDl[j], src[j * zs], q);
-                        dst[(j + 1) * zs] = q;
-                    }
-                } else {
+            // phase 1, in place: row j of the slot becomes Qc[j+1] = sum_{j'<=j} dtau_j' vol_j'
+            // (Qc[0] = 0 is implicit), two slabs per thread (float2).  Only the slabs some ray
+            // of the column can occupy while tau is in this chunk are built: z = w * t is
+            // extremal at the corners of [w_lo, w_hi] x [t_a, t_b]; one slab of margin on
+            // each side absorbs rounding.
+            float* stage = ring + (size_t)slot * C * zs;
+            const float cend = sB[cnt];
+            {
+                const float ta = chunk_start + tref, tb = cend + tref;
+                const float zlo = fminf(wlo * ta, wlo * tb), zhi = fmaxf(whi * ta, whi * tb);
+                int ilo = (int)floorf((zlo - lo2f) * ip2) - 1 + CBCT_ZPAD;
+                int ihi = (int)floorf((zhi - lo2f) * ip2) + 1 + CBCT_ZPAD;
+                ilo = max(ilo, CBCT_ZPAD - 1);
+                ihi = min(ihi, CBCT_ZPAD + nz);
+                const int zs2 = zs >> 1;
+                float2* col2 = reinterpret_cast<float2*>(stage);
+                for (int pi = (ilo >> 1) + threadIdx.x; pi <= (ihi >> 1); pi += nct) {
+                    float2 q = make_float2(0.0f, 0.0f);
+                    float2* cp = col2 + pi;
+#pragma unroll 4
                     for (int j = 0; j < cnt; ++j) {
-                        q = fmaf(sDl[j], src[j * zs], q);
-                        dst[(j + 1) * zs] = q;
+                        const float dl = sDl[j];
+                        const float2 x = cp[j * zs2];
+                        q.x = fmaf(dl, x.x, q.x);
+                        q.y = fmaf(dl, x.y, q.y);
+                        cp[j * zs2] = q;
                     }
                 }
             }
             named_bar(1, nct);
-            if (lane == 0) mbar_arrive(&empty[slot]);  // ring slot may be refilled
             // phase 2: per ray, the slab it ends in plus one correction per z crossing
-            const float cend = sB[cnt];
+            const float* last = stage + (cnt - 1) * zs;  // Qc[cnt]
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 RayState& s = st[r];
@@ -373,20 +381,21 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                     for (int step = C / 2; step > 0; step >>= 1)
                         if (m + step < cnt && sB[m + step] <= s.tz) m += step;
                     const float f = (s.tz - sB[m]) * sInv[m];
-                    const float* q0 = qc + m * zs;
-                    const float* q1 = q0 + zs;
+                    const float* q1 = stage + m * zs;          // Qc[m+1]
                     const int izn = s.iz + s.dz;
-                    const float ro = fmaf(f, q1[s.iz] - q0[s.iz], q0[s.iz]);
-                    const float rn = fmaf(f, q1[izn] - q0[izn], q0[izn]);
+                    const float q0o = m > 0 ? q1[-zs + s.iz] : 0.0f, q0n = m > 0 ? q1[-zs + izn] : 0.0f;
+                    const float ro = fmaf(f, q1[s.iz] - q0o, q0o);
+                    const float rn = fmaf(f, q1[izn] - q0n, q0n);
                     s.acc += ro - rn;
                     s.iz = izn;
                     s.jf += 1.0f;
                     s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
                 }
-                s.acc += qc[cnt * zs + s.iz];
+                s.acc += last[s.iz];
             }
             chunk_start = cend;
-            named_bar(1, nct);  // qc / sB reused by the next chunk
+            named_bar(1, nct);  // the slot (now Qc) and sB are reused
+            if (lane == 0) mbar_arrive(&empty[slot]);
         }
     }
 
@@ -422,15 +431,15 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
     if (p->proj_q && getenv("CBCT_PROJ_LDG") == nullptr && getenv("CBCT_PROJ_TMA") == nullptr) {
         const int Cq = p->proj_q_c;
         const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
-        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)(2 * Cq + Cq + 1) * p->zs * 4 +
+        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * Cq * p->zs * 4 +
                             (size_t)(3 * Cq + 1) * 4;
         const int nt = p->proj_threads + 32;
 #define LAUNCH_Q(R, CC)                                                                                        \
         do {                                                                                                   \
-            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                                             (int)smem));                                                       \
-            k_project_q<R, CC><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj,  \
-                                                      partials, (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2],     \
+            k_project_q<R, CC><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj, \
+                                                      partials, (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2],    \
                                                       p->pitch[2], p->flat_v, ent_cap, c0);                      \
         } while (0)
         switch (p->proj_rpt * 100 + Cq) {
