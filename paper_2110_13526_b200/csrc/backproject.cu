@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
 // checks this and otherwise uses k_bp_direct).  One lane per boundary; a warp
 // covers 32 boundaries = 31 voxels and exchanges G with its neighbour lane.
 
-// P[c][v] = sum_{v' < v} yw[c][v'], v = 0..nv+1 (P[c][nv+1] = P[c][nv]); yw = |r| * y.
+// P[c][v] = sum_{v' < v} yw[c][v'], v = 0..nv+1 (P[c][nv+1] = P[c][nv]); yw = |r| * y,
+// stored as pairs {P[v], P[v+1]}, v = 0..nv, so a lookup is one 8-byte load.
 // The straddling ray's own weight is recovered as P[v+1] - P[v] (it only scales
 // the straddle fraction F, so the fp32 cancellation there is harmless), which
 // halves the bytes per boundary lookup.  The flat row (if any) is kept out of P
@@ -188,7 +189,7 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
     if (c >= n_cols) return;
     const float rxy2 = (float)cols[c].rxy2;
     const float* yc = y + c * nv;
-    float* pc = pref + c * (int64_t)(nv + 2);
+    float2* pc = reinterpret_cast<float2*>(pref) + c * (int64_t)(nv + 1);  // {P[v], P[v+1]} pairs
     double carry = 0.0;
     for (int base = 0; base < nv; base += 32) {
         const int v = base + lane;
@@ -207,10 +208,10 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
             const double t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (v < nv) pc[v] = (float)(carry + incl - (double)yw);
+        if (v < nv) pc[v] = make_float2((float)(carry + incl - (double)yw), (float)(carry + incl));
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) pc[nv] = pc[nv + 1] = (float)carry;
+    if (lane == 0) pc[nv] = make_float2((float)carry, (float)carry);
 }
 
 template <int G, bool FLAT, bool TABLE>
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         __syncthreads();
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float* pyc = pyb + (size_t)(uint32_t)s_vu[k] * (uint32_t)(nv + 2);
+            const float2* pyc = reinterpret_cast<const float2*>(pyb) + (size_t)(uint32_t)s_vu[k] * (uint32_t)(nv + 1);
             asm("mov.b64 %0, %0;" : "+l"(pyc));  // keep the column base in a register (1 IMAD.WIDE per lookup)
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                 float W = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
                 W = sgn[g] != 0.0f ? fminf(W, wbnd[g]) : fmaxf(W, wbnd[g]);  // other side cannot overflow
                 const uint32_t vh = (uint32_t)(__float_as_int(__fadd_rd(W, 12582912.0f)) - magic);
-                const float P0 = __ldg(pyc + vh), P1 = __ldg(pyc + vh + 1);
+                const float2 PP = __ldg(pyc + vh);  // {P[vh], P[vh+1]}
+                const float P0 = PP.x, P1 = PP.y;
                 // Straddler (ray vh): fraction of [t_a, t_b] below z as one saturated FFMA
                 // (FMA pipe); below the mid-plane the table holds -inf for rz >= 0 rays, which
                 // saturates to 0 (such a ray cannot straddle a negative z).
@@ -352,7 +354,7 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
     if (mode == 1 && p->bp_boundary_ok && !precise) {
         float* pyb = scratch;
-        float* flatw = scratch + p->n_cols * (p->nv + 2);
+        float* flatw = scratch + p->n_cols * 2 * (p->nv + 1);
         const int64_t nthreads = p->n_cols * 32;
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v);

@@ -488,7 +488,7 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->max_cell_entries = p->max_cell_entries;
     info->table_bytes = (int64_t)p->table_bytes;
     info->proj_blocks = p->proj_blocks;
-    info->bp_scratch_floats = std::max<int64_t>(p->n_cols * (p->nv + 2) + p->n_cols, p->n_rays);
+    info->bp_scratch_floats = std::max<int64_t>(p->n_cols * 2 * (p->nv + 1) + p->n_cols, p->n_rays);
     info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
     info->bp_blocks = p->bp_blocks;
     return 0;
