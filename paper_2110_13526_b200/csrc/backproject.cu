@@ -175,21 +175,25 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
 // checks this and otherwise uses k_bp_direct).  One lane per boundary; a warp
 // covers 32 boundaries = 31 voxels and exchanges G with its neighbour lane.
 
-// P[c][v] = sum_{v' < v} yw[c][v'], v = 0..nv+1 (P[c][nv+1] = P[c][nv]); yw = |r| * y,
-// stored as pairs {P[v], P[v+1]}, v = 0..nv, so a lookup is one 8-byte load.
+// P[c][v] = sum_{v' < v} yw[c][v'], v = 0..nv (yw = |r| * y), padded past both detector
+// edges (P = 0 below, P[nv] above; v = -pad_lo .. nv + pad_hi + 1) so the backprojector
+// never clamps a row index.
 // The straddling ray's own weight is recovered as P[v+1] - P[v] (it only scales
 // the straddle fraction F, so the fp32 cancellation there is harmless), which
 // halves the bytes per boundary lookup.  The flat row (if any) is kept out of P
 // and stored in flatw[c].
 __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
                               const float* __restrict__ y, float* __restrict__ pref, float* __restrict__ flatw,
-                              int64_t n_cols, int nv, int flat_v) {
+                              int64_t n_cols, int nv, int flat_v, int pad_lo, int pad_hi) {
     const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (c >= n_cols) return;
     const float rxy2 = (float)cols[c].rxy2;
     const float* yc = y + c * nv;
-    float2* pc = reinterpret_cast<float2*>(pref) + c * (int64_t)(nv + 1);  // {P[v], P[v+1]} pairs
+    const int nvq = nv + 2 + pad_lo + pad_hi;
+    float* pc = pref + c * (int64_t)nvq;  // P[v] at row pad_lo + v
+    for (int k = lane; k < pad_lo; k += 32) pc[k] = 0.0f;
+    pc += pad_lo;
     double carry = 0.0;
     for (int base = 0; base < nv; base += 32) {
         const int v = base + lane;
@@ -208,10 +212,10 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
             const double t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
-        if (v < nv) pc[v] = make_float2((float)(carry + incl - (double)yw), (float)(carry + incl));
+        if (v < nv) pc[v] = (float)(carry + incl - (double)yw);
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) pc[nv] = make_float2((float)carry, (float)carry);
+    for (int k = nv + lane; k <= nv + pad_hi + 1; k += 32) pc[k] = (float)carry;
 }
 
 template <int G, bool FLAT, bool TABLE>
@@ -223,8 +227,8 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
                                                       const float* __restrict__ col_scale,
                                                       double* __restrict__ partials, int nv, int nz, int zs,
                                                       double lo2, double p2, double det00z, double pv, int nx,
-                                                      int row0, int row1) {
-    extern __shared__ float s_iw[];  // 2 x (nv + 1): 1/rz (pad 0); 1/rz for rz < 0, else -inf
+                                                      int row0, int row1, int pad_lo, int pad_hi) {
+    extern __shared__ float s_iw[];  // 2 x nvq rows: 1/rz (pad 0); 1/rz for rz < 0, else -inf
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
     const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
@@ -234,11 +238,13 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    float* s_iwn = s_iw + (nv + 1);
-    for (int k = threadIdx.x; k <= nv; k += blockDim.x) {
-        const float iw = k < nv ? invw[k] : 0.0f;
+    const int nvq = nv + 2 + pad_lo + pad_hi;
+    float* s_iwn = s_iw + nvq;
+    for (int k = threadIdx.x; k < nvq; k += blockDim.x) {
+        const int v = k - pad_lo;
+        const float iw = (v >= 0 && v < nv) ? invw[v] : 0.0f;
         s_iw[k] = iw;
-        s_iwn[k] = (k < nv && iw < 0.0f) ? iw : -INFINITY;
+        s_iwn[k] = (v >= 0 && v < nv && iw < 0.0f) ? iw : -INFINITY;
     }
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -247,13 +253,12 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         kb[g] = (warp + g * nwarps) * 31 + lane;  // boundary index (voxel below it is kb-1)
-        z[g] = (float)(lo2 + (double)kb[g] * p2);
+        z[g] = (float)(lo2 + (double)min(kb[g], nz) * p2);  // lanes past the top reuse it (unused)
         acc[g] = 0.0f;
         sgn[g] = z[g] >= 0.0f ? 1.0f : 0.0f;
         sgn2[g] = z[g] >= 0.0f ? 1.0f : -1.0f;
     }
-    const float* tbl[G];
-    float wbnd[G];
+    uint32_t tbase[G];
     // Row coordinate of a ray through height z at parameter t: v = z/(t pv) + c0,
     // c0 = -det00z/pv (= nv/2 - 1/2 without a principal-point offset).  c0 is split
     // into an integer and a fraction so the fp32 FFMA only carries z/(t pv) + frac:
@@ -263,15 +268,11 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     const double c0i = floor(c0d + 0.5);
     const float c0f = (float)(c0d - c0i);
     const int magic = 0x4B400000 - (int)c0i - 1;  // floor(W) + c0i + 1 via the 1.5*2^23 trick
-    const int c0ii = (int)c0i;
-    const float wlo = (float)(-c0i - 1.0), whi = (float)((double)nv - c0i - 0.5);
     const float fpv = (float)pv;
-    const float* __restrict__ pyb = pref;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        tbl[g] = sgn[g] != 0.0f ? s_iw : s_iwn;
-        wbnd[g] = sgn[g] != 0.0f ? whi : wlo;
-    }
+    for (int g = 0; g < G; ++g)  // shared address of row 0 of the lane's table minus 4 * magic (mod 2^32)
+        tbase[g] = (uint32_t)__cvta_generic_to_shared(sgn[g] != 0.0f ? s_iw : s_iwn) +
+                   4u * (uint32_t)(pad_lo - magic);
 
     for (int base = 0; base < ne; base += kChunk) {
         const int nch = min(kChunk, ne - base);
@@ -293,28 +294,30 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         __syncthreads();
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float2* pyc = reinterpret_cast<const float2*>(pyb) + (size_t)(uint32_t)s_vu[k] * (uint32_t)(nv + 1);
+            // the float->int magic offset is folded into the base: element address = base + bits
+            const float* pyc = pref + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq + pad_lo - (uint32_t)magic;
             asm("mov.b64 %0, %0;" : "+l"(pyc));  // keep the column base in a register (1 IMAD.WIDE per lookup)
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 // V(z): rays entirely below z, with t* = t_b above the mid-plane and t_a below
-                // (blended with the lane's up01 so no select sits on the ALU pipe).
-                float W = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
-                W = sgn[g] != 0.0f ? fminf(W, wbnd[g]) : fmaxf(W, wbnd[g]);  // other side cannot overflow
-                const uint32_t vh = (uint32_t)(__float_as_int(__fadd_rd(W, 12582912.0f)) - magic);
-                const float2 PP = __ldg(pyc + vh);  // {P[vh], P[vh+1]}
-                const float P0 = PP.x, P1 = PP.y;
+                // (blended with the lane's up01 so no select sits on the ALU pipe).  No row
+                // clamping: the prefix table is padded past both detector edges.
+                const float W = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
+                const uint32_t bits = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));  // vh + magic
+                // P[vh] and P[vh+1] (the second load hits the line the first brought to L1)
+                const float P0 = __ldg(pyc + bits), P1 = __ldg(pyc + bits + 1);
                 // Straddler (ray vh): fraction of [t_a, t_b] below z as one saturated FFMA
                 // (FMA pipe); below the mid-plane the table holds -inf for rz >= 0 rays, which
                 // saturates to 0 (such a ray cannot straddle a negative z).
-                const float iw = tbl[g][vh];
+                float iw;
+                asm("ld.shared.f32 %0, [%1];" : "=f"(iw) : "r"(tbase[g] + bits * 4u));
                 const float u = fmaf(z[g], iw, -t0.z);
                 // above: (u - t_a)/dt = u/dt - t_a/dt ; below: (t_b - u)/dt   (t_a/dt = t_b/dt - 1)
                 const float kap = fmaf(sgn[g], t1.z, t1.y);  // up: -t_a/dt, down: t_b/dt
                 const float f = __saturatef(fmaf(u, sgn2[g] * t1.x, kap));
-                const float Gv = t0.w * fmaf(f, P1 - P0, P0);
+                const float Gv = fmaf(f, P1 - P0, P0);  // unscaled; dt applied once below
                 const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
-                acc[g] += Gn - Gv;
+                acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
                 if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.w : 0.0f;
             }
         }
@@ -354,13 +357,14 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
     if (mode == 1 && p->bp_boundary_ok && !precise) {
         float* pyb = scratch;
-        float* flatw = scratch + p->n_cols * 2 * (p->nv + 1);
+        const int nvq = (int)p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi;
+        float* flatw = scratch + p->n_cols * nvq;
         const int64_t nthreads = p->n_cols * 32;
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
-                                                                           p->n_cols, (int)p->nv, p->flat_v);
+                                                                           p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi);
         CBCT_CHECK(cudaGetLastError());
         const bool table = true;  // the 1/rz tables beat rcp.approx (measured)
-        const size_t smem = 2 * (size_t)(p->nv + 1) * sizeof(float);
+        const size_t smem = 2 * (size_t)nvq * sizeof(float);
         const int64_t tiles = ((p->nx + 15) / 16) * ((row1 - row0 + 15) / 16);
         const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \
@@ -371,13 +375,13 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
                 k_bp_boundary<G, FL, true><<<grid, p->bpg_threads, smem, s>>>(                                 \
                     p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,  \
                     (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,  \
-                    (int)row0, (int)row1);                                                                               \
+                    (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi);                                                                               \
                 break;                                                                                         \
             }                                                                                                  \
             k_bp_boundary<G, FL, false><<<grid, p->bpg_threads, smem, s>>>(                                    \
                 p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
                 (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,      \
-                (int)row0, (int)row1);                                                                                   \
+                (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi);                                                                                   \
         } while (0)
         const bool fl = p->flat_v >= 0;
         switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {

@@ -400,6 +400,15 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
             const double wmax = fmax(fabs(det00z), fabs(det00z + (double)(g->nv - 1) * pv));
             // two rays can straddle one boundary only if |w| dt > pv t_a somewhere
             p->bp_boundary_ok = wmax * (double)mx < 0.9 * pv * (double)tmin_f;
+            // row range of W = z / (t pv) + c0 over the volume's boundaries (|z| <= zmax, t >= tmin):
+            // the prefix table is padded to cover it so the backprojector never clamps a row index
+            const double zmax = fmax(fabs(g->lo[2]), fabs(g->lo[2] + (double)g->nz * g->pitch[2]));
+            const double rr = tmin_f > 0.0f ? ceil(zmax / ((double)tmin_f * pv)) + 2.0 : 1e9;
+            const double c0i = floor(-det00z / pv + 0.5);
+            const double lo_need = rr + 2.0 - c0i, hi_need = c0i + rr + 3.0 - (double)g->nv;
+            if (rr > 1e6 || lo_need > 1e6 || hi_need > 1e6) p->bp_boundary_ok = false;
+            p->bp_pad_lo = p->bp_boundary_ok ? (int32_t)fmax(0.0, lo_need) + 1 : 0;
+            p->bp_pad_hi = p->bp_boundary_ok ? (int32_t)fmax(0.0, hi_need) + 1 : 0;
         }
         TRY(dev_alloc(&p->d_w, g->nv, &total));
         TRY(dev_alloc(&p->d_invw, g->nv, &total));
@@ -488,7 +497,8 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->max_cell_entries = p->max_cell_entries;
     info->table_bytes = (int64_t)p->table_bytes;
     info->proj_blocks = p->proj_blocks;
-    info->bp_scratch_floats = std::max<int64_t>(p->n_cols * 2 * (p->nv + 1) + p->n_cols, p->n_rays);
+    info->bp_scratch_floats =
+        std::max<int64_t>(p->n_cols * (p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi) + p->n_cols, p->n_rays);
     info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
     info->bp_blocks = p->bp_blocks;
     return 0;
