@@ -86,7 +86,7 @@ typedef struct cbct_plan_info {
     int32_t bp_blocks;         /* number of fp64 partials written by cbct_backproject */
     int64_t bp_scratch_floats; /* fp32 workspace cbct_backproject needs (scratch_proj) */
     int32_t bp_fast_path;      /* 1: mode-1 A^T uses the boundary-form kernel */
-    int32_t pad_;
+    int32_t bp_closed_form;    /* 1: its straddle fraction is the closed form (no 1/rz table) */
 } cbct_plan_info;
 
 /* ---- plan lifecycle ------------------------------------------------------ */

@@ -42,7 +42,7 @@ class PlanInfo(ctypes.Structure):
         ("n_columns", c_i64), ("n_intervals", c_i64), ("max_intervals", c_i64),
         ("max_cell_entries", c_i64), ("table_bytes", c_i64),
         ("proj_blocks", c_i32), ("bp_blocks", c_i32),
-        ("bp_scratch_floats", c_i64), ("bp_fast_path", c_i32), ("pad_", c_i32),
+        ("bp_scratch_floats", c_i64), ("bp_fast_path", c_i32), ("bp_closed_form", c_i32),
     ]
 
 

@@ -219,7 +219,7 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
 }
 
 template <int G, bool FLAT, bool TABLE>
-__global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict__ cell_off,
+__global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restrict__ cell_off,
                                                       const CellEntry* __restrict__ cell_ent,
                                                       const ColumnHeader* __restrict__ cols,
                                                       const float* __restrict__ invw, const float* __restrict__ pref,
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     const int ne = (int)(cell_off[cell + 1] - off);
     const int nvq = nv + 2 + pad_lo + pad_hi;
     float* s_iwn = s_iw + nvq;
-    for (int k = threadIdx.x; k < nvq; k += blockDim.x) {
+    for (int k = threadIdx.x; TABLE && k < nvq; k += blockDim.x) {
         const int v = k - pad_lo;
         const float iw = (v >= 0 && v < nv) ? invw[v] : 0.0f;
         s_iw[k] = iw;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
     }
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    float z[G], acc[G], sgn[G], sgn2[G];
+    float z[G], acc[G], sgn[G], sgn2[G], iz[G], sdn[G];
     int kb[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
         acc[g] = 0.0f;
         sgn[g] = z[g] >= 0.0f ? 1.0f : 0.0f;
         sgn2[g] = z[g] >= 0.0f ? 1.0f : -1.0f;
+        iz[g] = (float)(1.0 / (lo2 + (double)min(kb[g], nz) * p2));  // 1/z (z = 0: s saturates to 0)
+        sdn[g] = 1.0f - sgn[g];  // f = f_t above the mid-plane, 1 - f_t below
     }
     uint32_t tbase[G];
     // Row coordinate of a ray through height z at parameter t: v = z/(t pv) + c0,
@@ -283,39 +285,81 @@ __global__ void __launch_bounds__(1024) k_bp_boundary(const int64_t* __restrict_
             const float ta = ce.tau_a, tb = ce.tau_b, tr = h.t_ref;
             const float dt = tb - ta;
             const float idt = dt > 0.0f ? 1.0f / dt : 0.0f;
-            // {1/(t_a pv), 1/(t_b pv), t_ref, dt}, {1/dt, -t_a/dt, t_b/dt, flat-row weight}
-            const float ia = 1.0f / ((ta + tr) * fpv), ib = 1.0f / ((tb + tr) * fpv);
+            const float taa = ta + tr, tba = tb + tr;  // absolute ray parameters
+            // 1/(t_a pv) as a two-word fp32 (hi + lo) from fp64: the closed-form straddle
+            // fraction needs z / (t_a pv) to ~1e-9 relative (see the inner loop)
+            const double iad = 1.0 / (((double)ta + (double)tr) * pv);
+            const float ia = (float)iad, ia_lo = (float)(iad - (double)ia);
+            const float ib = (float)(1.0 / (((double)tb + (double)tr) * pv));
             // side-blended forms: value = below + up01 * (above - below), up01 in {0, 1} per lane
-            s_t0[k] = make_float4(ia, ib - ia, tr, dt);
-            s_t1[k] = make_float4(idt, tb * idt, -(ta + tb) * idt, FLAT ? flatw[ce.vu] : 0.0f);
+            if (TABLE) {
+                // {1/(t_a pv), 1/(t_b pv) - 1/(t_a pv), t_ref, dt}, {1/dt, -t_a/dt, t_b/dt, flat weight}
+                s_t0[k] = make_float4(ia, ib - ia, tr, dt);
+                s_t1[k] = make_float4(idt, tb * idt, -(ta + tb) * idt, FLAT ? flatw[ce.vu] : 0.0f);
+            } else {
+                // {ia (hi), ib - ia, kI = 1/(ia - ib) = pv t_a t_b / dt (from dt: no cancellation), dt},
+                // {eps = dt / t_a, ia (lo), 1 - eps, flat weight}
+                s_t0[k] = make_float4(ia, ib - ia, dt > 0.0f ? fpv * taa * tba / dt : 0.0f, dt);
+                s_t1[k] = make_float4(dt / taa, ia_lo, 1.0f - dt / taa, FLAT ? flatw[ce.vu] : 0.0f);
+            }
             s_vu[k] = ce.vu;
             s_fs[k] = FLAT ? h.flat_slab : 0;
         }
         __syncthreads();
+#pragma unroll 2  // two entries per trip: the next entry's loads overlap this entry's arithmetic
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
             // the float->int magic offset is folded into the base: element address = base + bits
             const float* pyc = pref + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq + pad_lo - (uint32_t)magic;
             asm("mov.b64 %0, %0;" : "+l"(pyc));  // keep the column base in a register (1 IMAD.WIDE per lookup)
+            // all lookups first, so the loads of every group are in flight before any use
+            float Wg[G], P0[G], P1[G];
+            uint32_t bg[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 // V(z): rays entirely below z, with t* = t_b above the mid-plane and t_a below
                 // (blended with the lane's up01 so no select sits on the ALU pipe).  No row
                 // clamping: the prefix table is padded past both detector edges.
-                const float W = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
-                const uint32_t bits = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));  // vh + magic
+                Wg[g] = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
+                bg[g] = (uint32_t)__float_as_int(__fadd_rd(Wg[g], 12582912.0f));  // vh + magic
                 // P[vh] and P[vh+1] (the second load hits the line the first brought to L1)
-                const float P0 = __ldg(pyc + bits), P1 = __ldg(pyc + bits + 1);
-                // Straddler (ray vh): fraction of [t_a, t_b] below z as one saturated FFMA
-                // (FMA pipe); below the mid-plane the table holds -inf for rz >= 0 rays, which
-                // saturates to 0 (such a ray cannot straddle a negative z).
-                float iw;
-                asm("ld.shared.f32 %0, [%1];" : "=f"(iw) : "r"(tbase[g] + bits * 4u));
-                const float u = fmaf(z[g], iw, -t0.z);
-                // above: (u - t_a)/dt = u/dt - t_a/dt ; below: (t_b - u)/dt   (t_a/dt = t_b/dt - 1)
-                const float kap = fmaf(sgn[g], t1.z, t1.y);  // up: -t_a/dt, down: t_b/dt
-                const float f = __saturatef(fmaf(u, sgn2[g] * t1.x, kap));
-                const float Gv = fmaf(f, P1 - P0, P0);  // unscaled; dt applied once below
+                P0[g] = __ldg(pyc + bg[g]);
+                P1[g] = __ldg(pyc + bg[g] + 1);
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint32_t bits = bg[g];
+                float f;
+                if (TABLE) {
+                    // Straddler (ray vh): fraction of [t_a, t_b] below z as one saturated FFMA
+                    // (FMA pipe); below the mid-plane the table holds -inf for rz >= 0 rays, which
+                    // saturates to 0 (such a ray cannot straddle a negative z).
+                    float iw;
+                    asm("ld.shared.f32 %0, [%1];" : "=f"(iw) : "r"(tbase[g] + bits * 4u));
+                    const float u = fmaf(z[g], iw, -t0.z);
+                    // above: (u - t_a)/dt = u/dt - t_a/dt ; below: (t_b - u)/dt   (t_a/dt = t_b/dt - 1)
+                    const float kap = fmaf(sgn[g], t1.z, t1.y);  // up: -t_a/dt, down: t_b/dt
+                    f = __saturatef(fmaf(u, sgn2[g] * t1.x, kap));
+                } else {
+                    // Straddler without a table.  W(t) = z/(t pv) + c0 is linear in 1/t, so the
+                    // straddler (row coordinate R = floor(W) + 1) meets height z at the 1/t-fraction
+                    //   s = (W_a - R) / (W_a - W_b) = (z ia + c0f - R) kI / z      (both sides)
+                    // of [t_a, t_b], and at the t-fraction  f_t = s / (1 + eps (1 - s)),
+                    // eps = dt / t_a, taken to first order (error <= eps^2/4; the plan selects this
+                    // form for eps <= 3e-3).  f = f_t above the mid-plane (a rising ray is below z
+                    // before t*), 1 - f_t below; rays that cannot straddle saturate to 0.
+                    // W_a - R is formed as fma(z, ia_lo, fma(z, ia_hi, -R) + c0f): every rounding
+                    // happens on an O(1) quantity, so f carries ~1e-7 absolute error instead of
+                    // the ~1e-4 an fp32 z/(t pv) near |W| ~ 300 rows would give.
+                    const float R = __int_as_float((int)bits) - 12582911.0f;  // floor(W) + 1, exact
+                    // s is saturated to [0, 1] first (the first-order f_t is only valid there; rays
+                    // that cannot straddle have s < 0 or > 1), then f_t = s (1 - eps + eps s).
+                    const float tail = fmaf(z[g], t1.y, c0f);  // z ia_lo + c0f, independent of R
+                    const float sv = __saturatef((fmaf(z[g], t0.x, -R) + tail) * (iz[g] * t0.z));
+                    const float h = fmaf(t1.x, sv, t1.z);            // 1 - eps + eps s
+                    f = fmaf(sgn2[g] * sv, h, sdn[g]);               // f_t above, 1 - f_t below
+                }
+                const float Gv = fmaf(f, P1[g] - P0[g], P0[g]);  // unscaled; dt applied once below
                 const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
                 acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
                 if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.w : 0.0f;
@@ -363,8 +407,10 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi);
         CBCT_CHECK(cudaGetLastError());
-        const bool table = true;  // the 1/rz tables beat rcp.approx (measured)
-        const size_t smem = 2 * (size_t)nvq * sizeof(float);
+        // closed-form straddle fraction unless the cells are long relative to the source distance
+        static const bool force_table = getenv("CBCT_BP_TABLE") != nullptr;
+        const bool table = force_table || !p->bp_closed_ok;
+        const size_t smem = table ? 2 * (size_t)nvq * sizeof(float) : 0;
         const int64_t tiles = ((p->nx + 15) / 16) * ((row1 - row0 + 15) / 16);
         const dim3 grid((unsigned)(tiles * 256));
 #define LAUNCH_G(G, FL)                                                                                        \

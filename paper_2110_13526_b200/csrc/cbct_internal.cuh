@@ -67,6 +67,7 @@ struct cbct_plan {
     int bpg_threads, bpg_groups;  // boundary-form backprojector shape
     bool bp_boundary_ok;          // at most one ray straddles any voxel boundary per crossing
     int32_t bp_pad_lo, bp_pad_hi; // rows of the ray-prefix table below 0 / above nv (no index clamping)
+    bool bp_closed_ok;            // eps = max dtau / min t small enough for the closed-form straddle
     float max_dtau;               // longest column/cell interval (ray parameter)
     int32_t proj_blocks, bp_blocks;
 };

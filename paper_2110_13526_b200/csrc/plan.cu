@@ -409,6 +409,8 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
             if (rr > 1e6 || lo_need > 1e6 || hi_need > 1e6) p->bp_boundary_ok = false;
             p->bp_pad_lo = p->bp_boundary_ok ? (int32_t)fmax(0.0, lo_need) + 1 : 0;
             p->bp_pad_hi = p->bp_boundary_ok ? (int32_t)fmax(0.0, hi_need) + 1 : 0;
+            // first-order closed form error <= eps^2 / 4 (backproject.cu)
+            p->bp_closed_ok = tmin_f > 0.0f && (double)mx <= 3e-3 * (double)tmin_f;
         }
         TRY(dev_alloc(&p->d_w, g->nv, &total));
         TRY(dev_alloc(&p->d_invw, g->nv, &total));
@@ -500,6 +502,7 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->bp_scratch_floats =
         std::max<int64_t>(p->n_cols * (p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi) + p->n_cols, p->n_rays);
     info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
+    info->bp_closed_form = (p->bp_boundary_ok && p->bp_closed_ok && !getenv("CBCT_BP_TABLE")) ? 1 : 0;
     info->bp_blocks = p->bp_blocks;
     return 0;
 }

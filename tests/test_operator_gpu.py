@@ -112,12 +112,28 @@ def test_config2_subsets_against_oracle(geom):
     else:
         vg, tr = baseline_geometry(256, 360, 512, 384, views=(10, 2), zslab=geom["zslab"])
     op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    # config-2 cells are short against the source distance: the boundary-form A^T with the
+    # closed-form straddle fraction (no 1/rz table) is the path under test here
+    assert op.info.bp_fast_path == 1 and op.info.bp_closed_form == 1
+    _check_random(op, ref)
+
+
+def _check_random(op, ref):
     x = np.random.default_rng(0).random(op.n).astype(np.float32).astype(np.float64)
     y = np.random.default_rng(1).standard_normal(op.m).astype(np.float32).astype(np.float64)
     got, want = op.project(_vol(op, x)).data, ref.project(x)
     assert max_rel(got, want) <= TOL, max_rel(got, want)
     got, want = op.backproject(_stack(op, y)).data, ref.backproject(y)
     assert max_rel(got, want) <= TOL, max_rel(got, want)
+
+
+def test_config3_views_against_oracle():
+    """BASELINE config 3 (512^3, 720 views, 616x480) on two views: the prefix-sum projector
+    at zs = 520 and the closed-form boundary backprojector at 0.43 mm voxels."""
+    vg, tr = baseline_geometry(512, 720, 616, 480, views=(100, 2))
+    op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    assert op.info.bp_fast_path == 1 and op.info.bp_closed_form == 1
+    _check_random(op, ref)
 
 
 def test_adjointness_and_linearity():

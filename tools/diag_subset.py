@@ -1,0 +1,28 @@
+"""A and A^T max-rel vs the oracle on a BASELINE config view subset:
+python tools/diag_subset.py N V nu nv view0 nviews"""
+import pathlib, sys
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+import numpy as np
+from _helpers import baseline_geometry, max_rel
+import paper_2110_13526_b200 as P
+from oracle import oracle as O
+
+N, V, nu, nv, v0, k = (int(a) for a in sys.argv[1:7])
+vg, tr = baseline_geometry(N, V, nu, nv, views=(v0, k))
+op, ref = P.CbctOperator(vg, tr), O.OracleOperator(vg, tr)
+x = np.random.default_rng(0).random(op.n).astype(np.float32).astype(np.float64)
+y = np.random.default_rng(1).standard_normal(op.m).astype(np.float32).astype(np.float64)
+a = op.project(P.Volume(vg, x.reshape(vg.nx, vg.ny, vg.nz) if False else x)).data if False else None
+got = op.project(P.operator.InternalVolume(vg, op.volume_to_internal(x))).data if False else None
+import torch
+xa = op.project(P.Volume(vg, x)).data
+xa = xa.cpu().numpy() if hasattr(xa, "cpu") else np.asarray(xa)
+ya = op.backproject(P.ProjectionStack(tr, y)).data
+ya = ya.cpu().numpy() if hasattr(ya, "cpu") else np.asarray(ya)
+rp, rb = ref.project(x), ref.backproject(y)
+e = np.abs(ya.ravel() - rb.ravel())
+i = int(np.argmax(e))
+print(f"closed={op.info.bp_closed_form} A maxrel {max_rel(xa, rp):.3e}  AT maxrel {max_rel(ya, rb):.3e} "
+      f"l2 {np.linalg.norm(e) / np.linalg.norm(rb):.3e} worst voxel {np.unravel_index(i, (vg.nx, vg.ny, vg.nz))} "
+      f"ref {rb.ravel()[i]:.5e} got {ya.ravel()[i]:.5e}")
