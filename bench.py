@@ -111,6 +111,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def committed_traffic(cfg: int) -> dict:
+    """Per-launch DRAM bytes of the hot kernels from the committed ncu capture (profiles/traffic_r1.json)."""
+    try:
+        with open(ROOT / "profiles" / "traffic_r1.json") as f:
+            return json.load(f).get(f"config{cfg}", {})
+    except (OSError, ValueError):
+        return {}
+
+
 # ------------------------------------------------------------------ CPU legs --
 def cpu_sample(cfg: int, nviews: int = None, threads: int = 0):
     """Reference algorithm (oracle port, C+OpenMP, fp64) on a contiguous view sample of
@@ -291,9 +300,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     nnz = NNZ[cfg]
     dom, t_dom = ("A^T", t_at) if t_at >= t_a else ("A", t_a)
     achieved = SLOTS_PER_NNZ * nnz / (t_dom * 1e-3)
-    roof = {"bound": "issue", "kernel": f"{dom} ({'k_backproject' if dom == 'A^T' else 'k_project'})",
+    kname = {"A^T": "k_bp_boundary", "A": "k_project_q"}[dom]
+    traffic = committed_traffic(cfg)
+    roof = {"bound": "issue", "kernel": f"{dom} ({kname})",
             "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
-            "traffic": None,
+            "traffic": traffic.get(kname), "traffic_unit": "B per launch (DRAM read + write, ncu)",
+            "traffic_A": traffic.get("k_project_q"),
             "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
                           f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
             "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
