@@ -30,6 +30,11 @@ struct Tri {  // staged per-crossing data
 };
 
 constexpr int kChunk = 256;
+#ifdef CBCT_BP_SINGLE
+constexpr int kPrefWords = 1;  // ray-prefix table: P[v]
+#else
+constexpr int kPrefWords = 2;  // ray-prefix table: {P[v], yw[v]} pairs
+#endif
 
 // Cells are visited in 16x16 tiles so concurrently resident CTAs share the
 // detector columns they read (L2 locality of the prefix arrays).
@@ -191,8 +196,13 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
     const float rxy2 = (float)cols[c].rxy2;
     const float* yc = y + c * nv;
     const int nvq = nv + 2 + pad_lo + pad_hi;
+#ifdef CBCT_BP_SINGLE
     float* pc = pref + c * (int64_t)nvq;  // P[v] at row pad_lo + v
     for (int k = lane; k < pad_lo; k += 32) pc[k] = 0.0f;
+#else
+    float2* pc = reinterpret_cast<float2*>(pref) + c * (int64_t)nvq;  // {P[v], yw[v]} at row pad_lo + v
+    for (int k = lane; k < pad_lo; k += 32) pc[k] = make_float2(0.0f, 0.0f);
+#endif
     pc += pad_lo;
     double carry = 0.0;
     for (int base = 0; base < nv; base += 32) {
@@ -212,10 +222,18 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
             const double t = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t;
         }
+#ifdef CBCT_BP_SINGLE
         if (v < nv) pc[v] = (float)(carry + incl - (double)yw);
+#else
+        if (v < nv) pc[v] = make_float2((float)(carry + incl - (double)yw), yw);
+#endif
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
+#ifdef CBCT_BP_SINGLE
     for (int k = nv + lane; k <= nv + pad_hi + 1; k += 32) pc[k] = (float)carry;
+#else
+    for (int k = nv + lane; k <= nv + pad_hi + 1; k += 32) pc[k] = make_float2((float)carry, 0.0f);
+#endif
 }
 
 template <int G, bool FLAT, bool TABLE>
@@ -310,7 +328,12 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
             // the float->int magic offset is folded into the base: element address = base + bits
+#ifdef CBCT_BP_SINGLE
             const float* pyc = pref + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq + pad_lo - (uint32_t)magic;
+#else
+            const float2* pyc = reinterpret_cast<const float2*>(pref) + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq +
+                                pad_lo - (uint32_t)magic;
+#endif
             asm("mov.b64 %0, %0;" : "+l"(pyc));  // keep the column base in a register (1 IMAD.WIDE per lookup)
             // all lookups first, so the loads of every group are in flight before any use
             float Wg[G], P0[G], P1[G];
@@ -322,9 +345,15 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
                 // clamping: the prefix table is padded past both detector edges.
                 Wg[g] = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
                 bg[g] = (uint32_t)__float_as_int(__fadd_rd(Wg[g], 12582912.0f));  // vh + magic
+#ifdef CBCT_BP_SINGLE
                 // P[vh] and P[vh+1] (the second load hits the line the first brought to L1)
                 P0[g] = __ldg(pyc + bg[g]);
-                P1[g] = __ldg(pyc + bg[g] + 1);
+                P1[g] = __ldg(pyc + bg[g] + 1) - P0[g];  // yw[vh]
+#else
+                const float2 py = __ldg(pyc + bg[g]);  // {P[vh], yw[vh]}: one 8-byte load
+                P0[g] = py.x;
+                P1[g] = py.y;
+#endif
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
                     const float h = fmaf(t1.x, sv, t1.z);            // 1 - eps + eps s
                     f = fmaf(sgn2[g] * sv, h, sdn[g]);               // f_t above, 1 - f_t below
                 }
-                const float Gv = fmaf(f, P1[g] - P0[g], P0[g]);  // unscaled; dt applied once below
+                const float Gv = fmaf(f, P1[g], P0[g]);  // P[vh] + f yw[vh]; dt applied once below
                 const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
                 acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
                 if (FLAT) acc[g] += (kb[g] == s_fs[k]) ? t0.w * t1.w : 0.0f;
@@ -402,7 +431,7 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     if (mode == 1 && p->bp_boundary_ok && !precise) {
         float* pyb = scratch;
         const int nvq = (int)p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi;
-        float* flatw = scratch + p->n_cols * nvq;
+        float* flatw = scratch + p->n_cols * nvq * kPrefWords;
         const int64_t nthreads = p->n_cols * 32;
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
                                                                            p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi);

@@ -500,7 +500,7 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->table_bytes = (int64_t)p->table_bytes;
     info->proj_blocks = p->proj_blocks;
     info->bp_scratch_floats =
-        std::max<int64_t>(p->n_cols * (p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi) + p->n_cols, p->n_rays);
+        std::max<int64_t>(p->n_cols * 2 * (p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi) + p->n_cols, p->n_rays);
     info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
     info->bp_closed_form = (p->bp_boundary_ok && p->bp_closed_ok && !getenv("CBCT_BP_TABLE")) ? 1 : 0;
     info->bp_blocks = p->bp_blocks;

@@ -272,6 +272,20 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Guard-padded slab range [x, y] that some ray of a column can occupy while tau is in
+// [tau_a, tau_b]: z = w t is extremal at the corners of [w_lo, w_hi] x [t_a, t_b]; one slab of
+// margin on each side absorbs rounding.  Producer and consumers evaluate it identically.
+__device__ __forceinline__ int2 chunk_slabs(float tau_a, float tau_b, float tref, float wlo, float whi, float lo2f,
+                                            float ip2, int nz) {
+    const float ta = tau_a + tref, tb = tau_b + tref;
+    const float zlo = fminf(wlo * ta, wlo * tb), zhi = fmaxf(whi * ta, whi * tb);
+    const int ilo = (int)floorf((zlo - lo2f) * ip2) - 1 + CBCT_ZPAD;
+    const int ihi = (int)floorf((zhi - lo2f) * ip2) + 1 + CBCT_ZPAD;
+    // both ends clamped into [guard below, guard above]: the window is never empty and always
+    // holds the guard slab a ray outside the volume sits in (reads a prefix of zeros)
+    return make_int2(min(max(ilo, CBCT_ZPAD - 1), CBCT_ZPAD + nz), min(max(ihi, CBCT_ZPAD - 1), CBCT_ZPAD + nz));
+}
+
 template <int RPT, int C>
 __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restrict__ cols,
                                                    const int64_t* __restrict__ col_off,
@@ -312,17 +326,21 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     __syncthreads();
 
     const int nch = (M + C - 1) / C;
-    const uint32_t col_bytes = (uint32_t)zs * 4u;
     if (producer) {
+        // stage only the 16-B-aligned slab window the chunk's rays can reach (the cone bound)
         for (int i = 0; i < nch; ++i) {
             const int slot = i & 1, round = i >> 1;
             if (round > 0) mbar_wait_backoff(&empty[slot], (round - 1) & 1);
             const int m0 = i * C, cnt = min(C, M - m0);
-            if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * col_bytes);
+            const int2 sl = chunk_slabs(i == 0 ? h.tau_start : s_ent[m0 - 1].x, s_ent[m0 + cnt - 1].x, tref, wlo, whi,
+                                        lo2f, ip2, nz);
+            const int lo4 = sl.x & ~3, hi4 = (sl.y + 4) & ~3;
+            const uint32_t bytes = (uint32_t)(hi4 - lo4) * 4u;
+            if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * bytes);
             __syncwarp();
             for (int j = lane; j < cnt; j += 32)
-                bulk_g2s(ring + ((size_t)slot * C + j) * zs, vol + (uint32_t)__float_as_int(s_ent[m0 + j].y),
-                         col_bytes, &full[slot]);
+                bulk_g2s(ring + ((size_t)slot * C + j) * zs + lo4,
+                         vol + (uint32_t)(__float_as_int(s_ent[m0 + j].y) + lo4), bytes, &full[slot]);
         }
     } else {
         float chunk_start = h.tau_start;
@@ -341,19 +359,14 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             mbar_wait(&full[slot], round & 1);
             named_bar(1, nct);  // sB / sDl visible
             // phase 1, in place: row j of the slot becomes Qc[j+1] = sum_{j'<=j} dtau_j' vol_j'
-            // (Qc[0] = 0 is implicit), two slabs per thread (float2).  Only the slabs some ray
-            // of the column can occupy while tau is in this chunk are built: z = w * t is
-            // extremal at the corners of [w_lo, w_hi] x [t_a, t_b]; one slab of margin on
-            // each side absorbs rounding.
+            // (Qc[0] = 0 is implicit), two slabs per thread (float2), only over the slabs some
+            // ray of the column can occupy while tau is in this chunk (chunk_slabs; the producer
+            // staged exactly that window).
             float* stage = ring + (size_t)slot * C * zs;
             const float cend = sB[cnt];
             {
-                const float ta = chunk_start + tref, tb = cend + tref;
-                const float zlo = fminf(wlo * ta, wlo * tb), zhi = fmaxf(whi * ta, whi * tb);
-                int ilo = (int)floorf((zlo - lo2f) * ip2) - 1 + CBCT_ZPAD;
-                int ihi = (int)floorf((zhi - lo2f) * ip2) + 1 + CBCT_ZPAD;
-                ilo = max(ilo, CBCT_ZPAD - 1);
-                ihi = min(ihi, CBCT_ZPAD + nz);
+                const int2 sl = chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
+                const int ilo = sl.x, ihi = sl.y;
                 const int zs2 = zs >> 1;
                 float2* col2 = reinterpret_cast<float2*>(stage);
                 for (int pi = (ilo >> 1) + threadIdx.x; pi <= (ihi >> 1); pi += nct) {
