@@ -211,9 +211,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     vg, tr = geometry(cfg)
     t_setup = time.perf_counter()
     op = P.CbctOperator(vg, tr, device=dev)
-    truth = P.generate_phantom(P.shepp_logan_3d(), vg)
-    x_t = torch.from_numpy(truth.data).to(dev)
-    b_int = op.project(P.Volume(vg, x_t), internal=True).data  # inverse crime b = A phantom (fp32, device)
+    x_int = op.phantom_internal(P.shepp_logan_3d())  # device voxelizer (bit-identical to generate_phantom)
+    b_int = op.new_projections()
+    op.project_internal(x_int, b_int)  # inverse crime b = A phantom (fp32, device)
     b = P.operator.InternalProjections(tr, b_int)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
@@ -353,7 +353,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
     comm = TorchComm()
     sop = ShardedOperator(vg, tr, comm, device=dev)
     op = sop.op
-    truth = op.volume_to_internal(P.generate_phantom(P.shepp_logan_3d(), vg).data)
+    truth = op.phantom_internal(P.shepp_logan_3d())
     b_full = op.new_projections()
     op.project_internal(truth, b_full)  # inverse crime b = A phantom; each rank keeps its view block
     b_local = torch.zeros(sop.m_loc, device=dev)

@@ -161,6 +161,18 @@ int cbct_fill(int64_t n, float* x, float value, void* stream);
 /* Fill a volume's interior with value and its guard slices with 0. */
 int cbct_fill_volume(const cbct_plan* plan, float* vol, float value, void* stream);
 
+/* ---- phantom voxelizer ------------------------------- */
+/* Replaces generate_phantom (phantom.py:87-106): sum of the intensities of the
+ * ellipsoids containing each voxel centre (phantom.py:78-84), bit-identical to the
+ * host generator.  `ellipsoids` is a DEVICE array of n_ell x 16 doubles per
+ * ellipsoid: cx cy cz, semi-axes a b c, the row-major 3x3 rotation of
+ * Ellipsoid.rotation() (phantom.py:37-40), intensity.
+ * cbct_phantom writes the plan's device volume layout (guards zeroed);
+ * cbct_phantom_ref writes the reference layout (nz, ny, nx), x fastest, fp32. */
+int cbct_phantom(const cbct_plan* plan, const double* ellipsoids, int n_ell, float* vol, void* stream);
+int cbct_phantom_ref(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, float* out,
+                     void* stream);
+
 /* ---- reference-signature entry points (host fp64, reference layouts) ------ */
 /* Drop-in for _project_kernel (operator.py:190-206). */
 int cbct_ref_project(const double* vol, double* out, const double* srcs, const double* det00,

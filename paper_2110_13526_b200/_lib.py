@@ -70,6 +70,8 @@ SIGNATURES = {
     "cbct_clip": (c_i32, [c_p, c_p, c_f32, c_f32, c_p]),
     "cbct_fill": (c_i32, [c_i64, c_p, c_f32, c_p]),
     "cbct_fill_volume": (c_i32, [c_p, c_p, c_f32, c_p]),
+    "cbct_phantom": (c_i32, [c_p, c_p, c_i32, c_p, c_p]),
+    "cbct_phantom_ref": (c_i32, [c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p]),
     "cbct_ref_project": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,
                                  c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64, c_i64, c_i64]),
     "cbct_ref_backproject": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,

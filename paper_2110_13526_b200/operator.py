@@ -176,6 +176,18 @@ class CbctOperator:
         call("cbct_volume_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
         return out
 
+    def phantom_internal(self, ellipsoids, out=None) -> torch.Tensor:
+        """generate_phantom(ellipsoids, vol_geom) voxelized on the device straight into the
+        device layout (csrc/phantom.cu; bit-identical to the host generator rounded to fp32)."""
+        from .phantom import _device_params
+
+        ellipsoids = list(ellipsoids)
+        out = self.new_volume() if out is None else out
+        params = _device_params(ellipsoids, self.device)
+        call("cbct_phantom", self._plan, _ptr(params) if ellipsoids else None, len(ellipsoids), _ptr(out),
+             self._stream())
+        return out
+
     def volume_from_internal(self, t: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
         out = torch.empty(self.n, dtype=dtype, device=self.device)
         call("cbct_volume_from_internal", self._plan, _ptr(t), _ptr(out), int(dtype == torch.float64),

@@ -117,3 +117,16 @@ def test_containers_coerce_like_reference():
     tr = make_circular_trajectory(100, 200, 2, 0, 1, DetectorGeometry(3, 2))
     s = ProjectionStack(tr)
     assert s.data.shape == (12,) and s.as_3d().shape == (2, 2, 3)
+
+
+def test_ellipsoid_params_pack_reference_rotations():
+    """Device voxelizer input: one row per ellipsoid, R exactly Ellipsoid.rotation()."""
+    import paper_2110_13526_b200 as P
+
+    ells = P.shepp_logan_3d()
+    prm = P.phantom.ellipsoid_params(ells)
+    assert prm.shape == (10, 16) and prm.dtype == np.float64
+    for row, e in zip(prm, ells):
+        assert tuple(row[0:3]) == tuple(e.center) and tuple(row[3:6]) == tuple(e.semi_axes)
+        assert np.array_equal(row[6:15].reshape(3, 3), e.rotation()) and row[15] == e.intensity
+    assert P.phantom.ellipsoid_params([]).shape == (0, 16)

@@ -13,9 +13,6 @@ vg, tr = baseline_geometry(N, V, nu, nv, views=(v0, k))
 op, ref = P.CbctOperator(vg, tr), O.OracleOperator(vg, tr)
 x = np.random.default_rng(0).random(op.n).astype(np.float32).astype(np.float64)
 y = np.random.default_rng(1).standard_normal(op.m).astype(np.float32).astype(np.float64)
-a = op.project(P.Volume(vg, x.reshape(vg.nx, vg.ny, vg.nz) if False else x)).data if False else None
-got = op.project(P.operator.InternalVolume(vg, op.volume_to_internal(x))).data if False else None
-import torch
 xa = op.project(P.Volume(vg, x)).data
 xa = xa.cpu().numpy() if hasattr(xa, "cpu") else np.asarray(xa)
 ya = op.backproject(P.ProjectionStack(tr, y)).data

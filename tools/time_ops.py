@@ -14,7 +14,7 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 vg, tr = bench.geometry(cfg)
 op = P.CbctOperator(vg, tr)
-x = op.volume_to_internal(P.generate_phantom(P.shepp_logan_3d(), vg).data)
+x = op.phantom_internal(P.shepp_logan_3d())
 p = op.new_projections()
 r = op.new_volume()
 scr = op.new_bp_scratch()
