@@ -62,7 +62,7 @@ struct cbct_plan {
     // launch shapes
     int proj_threads, proj_rpt;
     int proj_tma, proj_tma_k, proj_tma_stages;  // TMA-staged projector shape
-    int proj_q, proj_q_c;                       // column prefix-sum projector (chunk of C cells)
+    int proj_q, proj_q_c, proj_q_zr;            // column prefix-sum projector (chunk of C cells, zero row)
     int bp_threads, bp_zpt;
     int bpg_threads, bpg_groups;  // boundary-form backprojector shape
     bool bp_boundary_ok;          // at most one ray straddles any voxel boundary per crossing

@@ -440,11 +440,18 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         p->proj_tma = smem <= 200 * 1024 ? 1 : 0;
         // prefix-sum projector: 2 ring stages + Qc of C cells, ~<= 64 KB
         const int64_t per_c = 2 * col_bytes;  // two ring slots; the prefix is built in place
+        // chunk of 16 cells; per-slot zero row (Qc[0]) only if the CTA still fits ~76 KB, i.e.
+        // 3 CTAs per SM (measured: config 2 16+zr 10.3 ms, 16 11.1 ms, 8 14.6 ms; config 3
+        // 16 85 ms, 16+zr 103 ms, 12+zr 92 ms)
+        auto qsm = [&](int cc, int zr) {
+            return 32 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + (2 * cc + 33) * 4;
+        };
         int cq = 16;
-        while (cq > 8 && per_c * cq > 72 * 1024) cq >>= 1;
         if (const char* e = getenv("CBCT_PROJ_Q_C")) cq = atoi(e);
         p->proj_q_c = cq;
-        const int64_t qsmem = 32 + (p->max_intervals + 3) * 8 + per_c * cq + (3 * cq + 1) * 4;
+        p->proj_q_zr = qsm(cq, 1) <= 76 * 1024 ? 1 : 0;
+        if (const char* e = getenv("CBCT_PROJ_Q_ZR")) p->proj_q_zr = atoi(e) ? 1 : 0;
+        const int64_t qsmem = qsm(cq, p->proj_q_zr);
         // the slab-parallel prefix pays off unless z slabs far outnumber rays (measured: config 1
         // 0.11 vs 0.22 ms, config 2 11.0 vs 15.0 ms, config 3 86 vs 115 ms against the TMA walk)
         p->proj_q = (qsmem <= 220 * 1024 && (double)g->nv >= 0.5 * (double)zs) ? 1 : 0;

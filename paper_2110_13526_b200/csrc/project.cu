@@ -286,7 +286,7 @@ __device__ __forceinline__ int2 chunk_slabs(float tau_a, float tau_b, float tref
     return make_int2(min(max(ilo, CBCT_ZPAD - 1), CBCT_ZPAD + nz), min(max(ihi, CBCT_ZPAD - 1), CBCT_ZPAD + nz));
 }
 
-template <int RPT, int C>
+template <int RPT, int C, bool ZR>
 __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restrict__ cols,
                                                    const int64_t* __restrict__ col_off,
                                                    const float2* __restrict__ col_ent, const double* __restrict__ wtab,
@@ -297,20 +297,28 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
     uint64_t* empty = full + 2;                               // [2]
     float2* s_ent = reinterpret_cast<float2*>(smem_raw + 32);
-    float* ring = reinterpret_cast<float*>(s_ent + ent_cap);  // [2][C][zs]: staged columns, then Qc in place
-    float* sB = ring + 2 * C * zs;                             // [C+1] interval starts (+ chunk end)
-    float* sInv = sB + (C + 1);                                // [C]   1/dtau
-    float* sDl = sInv + C;                                     // [C]   dtau
+    // ZR: [2][C+1][zs], row 0 of a slot is Qc[0] = 0 (never written after init) and rows
+    // 1..cnt receive the staged cell columns; !ZR: [2][C][zs] (one row less per slot, when the
+    // extra rows would cost a resident CTA) and Qc[0] = 0 is a predicated load.  Phase 1 turns
+    // the staged rows into Qc[1..cnt] in place.
+    constexpr int RZ = ZR ? 1 : 0;
+    float* ring = reinterpret_cast<float*>(s_ent + ent_cap);
+    constexpr int PC = C <= 8 ? 8 : (C <= 16 ? 16 : 32);  // power-of-two search span
+    float* sB = ring + 2 * (C + RZ) * zs;  // [PC+1] interval starts, chunk end, then +inf padding
+    float* sInv = sB + (PC + 1);          // [C]   1/dtau
+    float* sDl = sInv + C;                // [C]   dtau
     const int nwc = (blockDim.x >> 5) - 1;
     const int nct = nwc * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = warp == nwc;
+    const int slot_elems = (C + RZ) * zs;
 
     const int64_t c = c0 + blockIdx.x;  // detector column (view * nu + u)
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
     for (int k = threadIdx.x; k < M; k += blockDim.x) s_ent[k] = col_ent[off + k];
+    for (int k = threadIdx.x; ZR && k < zs; k += blockDim.x) ring[k] = ring[slot_elems + k] = 0.0f;
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full[i], 1);
@@ -332,23 +340,24 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             const int slot = i & 1, round = i >> 1;
             if (round > 0) mbar_wait_backoff(&empty[slot], (round - 1) & 1);
             const int m0 = i * C, cnt = min(C, M - m0);
-            const int2 sl = chunk_slabs(i == 0 ? h.tau_start : s_ent[m0 - 1].x, s_ent[m0 + cnt - 1].x, tref, wlo, whi,
-                                        lo2f, ip2, nz);
+            const int2 sl = chunk_slabs(i == 0 ? h.tau_start : s_ent[m0 - 1].x, s_ent[m0 + cnt - 1].x, tref, wlo,
+                                        whi, lo2f, ip2, nz);
             const int lo4 = sl.x & ~3, hi4 = (sl.y + 4) & ~3;
             const uint32_t bytes = (uint32_t)(hi4 - lo4) * 4u;
+            float* dst = ring + (size_t)slot * slot_elems + RZ * zs + lo4;
             if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * bytes);
             __syncwarp();
             for (int j = lane; j < cnt; j += 32)
-                bulk_g2s(ring + ((size_t)slot * C + j) * zs + lo4,
-                         vol + (uint32_t)(__float_as_int(s_ent[m0 + j].y) + lo4), bytes, &full[slot]);
+                bulk_g2s(dst + (size_t)j * zs, vol + (uint32_t)(__float_as_int(s_ent[m0 + j].y) + lo4), bytes,
+                         &full[slot]);
         }
     } else {
         float chunk_start = h.tau_start;
         for (int i = 0; i < nch; ++i) {
             const int slot = i & 1, round = i >> 1;
             const int m0 = i * C, cnt = min(C, M - m0);
-            for (int k = threadIdx.x; k <= cnt; k += nct) {
-                const float bb = k == 0 ? chunk_start : s_ent[m0 + k - 1].x;
+            for (int k = threadIdx.x; k <= PC; k += nct) {
+                const float bb = k == 0 ? chunk_start : (k <= cnt ? s_ent[m0 + k - 1].x : INFINITY);
                 sB[k] = bb;
                 if (k < cnt) {
                     const float e = s_ent[m0 + k].x;
@@ -358,18 +367,17 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             }
             mbar_wait(&full[slot], round & 1);
             named_bar(1, nct);  // sB / sDl visible
-            // phase 1, in place: row j of the slot becomes Qc[j+1] = sum_{j'<=j} dtau_j' vol_j'
-            // (Qc[0] = 0 is implicit), two slabs per thread (float2), only over the slabs some
-            // ray of the column can occupy while tau is in this chunk (chunk_slabs; the producer
-            // staged exactly that window).
-            float* stage = ring + (size_t)slot * C * zs;
+            // phase 1, in place: row j+1 of the slot becomes Qc[j+1] = sum_{j'<=j} dtau_j' vol_j'
+            // (row 0 = Qc[0] = 0), two slabs per thread (float2), only over the slabs some ray of
+            // the column can occupy while tau is in this chunk (chunk_slabs; the producer staged
+            // exactly that window).
+            float* stage = ring + (size_t)slot * slot_elems;
             const float cend = sB[cnt];
             {
                 const int2 sl = chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
-                const int ilo = sl.x, ihi = sl.y;
                 const int zs2 = zs >> 1;
-                float2* col2 = reinterpret_cast<float2*>(stage);
-                for (int pi = (ilo >> 1) + threadIdx.x; pi <= (ihi >> 1); pi += nct) {
+                float2* col2 = reinterpret_cast<float2*>(stage + RZ * zs);
+                for (int pi = (sl.x >> 1) + threadIdx.x; pi <= (sl.y >> 1); pi += nct) {
                     float2 q = make_float2(0.0f, 0.0f);
                     float2* cp = col2 + pi;
 #pragma unroll 4
@@ -383,23 +391,31 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                 }
             }
             named_bar(1, nct);
-            // phase 2: per ray, the slab it ends in plus one correction per z crossing
-            const float* last = stage + (cnt - 1) * zs;  // Qc[cnt]
+            // phase 2: per ray, the slab it ends in plus one correction per z crossing.  The
+            // interval search needs no bounds checks (sB is +inf-padded past the chunk end, which
+            // the crossing is before).
+            const float* last = stage + (cnt - 1 + RZ) * zs;  // Qc[cnt]
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 RayState& s = st[r];
                 while (s.tz < cend) {
                     int m = 0;
 #pragma unroll
-                    for (int step = C / 2; step > 0; step >>= 1)
-                        if (m + step < cnt && sB[m + step] <= s.tz) m += step;
+                    for (int step = PC / 2; step > 0; step >>= 1)
+                        if (sB[m + step] <= s.tz) m += step;
                     const float f = (s.tz - sB[m]) * sInv[m];
-                    const float* q1 = stage + m * zs;          // Qc[m+1]
+                    const float* q1 = stage + (m + RZ) * zs;  // Qc[m+1]
                     const int izn = s.iz + s.dz;
-                    const float q0o = m > 0 ? q1[-zs + s.iz] : 0.0f, q0n = m > 0 ? q1[-zs + izn] : 0.0f;
-                    const float ro = fmaf(f, q1[s.iz] - q0o, q0o);
-                    const float rn = fmaf(f, q1[izn] - q0n, q0n);
-                    s.acc += ro - rn;
+                    float a0, b0;
+                    if (ZR) {
+                        a0 = q1[s.iz - zs];
+                        b0 = q1[izn - zs];
+                    } else {
+                        a0 = m > 0 ? q1[s.iz - zs] : 0.0f;
+                        b0 = m > 0 ? q1[izn - zs] : 0.0f;
+                    }
+                    const float a1 = q1[s.iz], b1 = q1[izn];
+                    s.acc += fmaf(f, a1 - a0, a0) - fmaf(f, b1 - b0, b0);
                     s.iz = izn;
                     s.jf += 1.0f;
                     s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
@@ -444,29 +460,38 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
     if (p->proj_q && getenv("CBCT_PROJ_LDG") == nullptr && getenv("CBCT_PROJ_TMA") == nullptr) {
         const int Cq = p->proj_q_c;
         const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
-        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * Cq * p->zs * 4 +
-                            (size_t)(3 * Cq + 1) * 4;
+        const int zr = p->proj_q_zr;
+        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * (Cq + zr) * p->zs * 4 +
+                            (size_t)(2 * Cq + 33) * 4;
         const int nt = p->proj_threads + 32;
+#define LAUNCH_Q2(R, CC, Z)                                                                                    \
+        do {                                                                                                   \
+            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                            (int)smem));                                                       \
+            k_project_q<R, CC, Z><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol,    \
+                                                         proj, partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
+                                                         p->lo[2], p->pitch[2], p->flat_v, ent_cap, c0);        \
+        } while (0)
 #define LAUNCH_Q(R, CC)                                                                                        \
         do {                                                                                                   \
-            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                            (int)smem));                                                       \
-            k_project_q<R, CC><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol, proj, \
-                                                      partials, (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2],    \
-                                                      p->pitch[2], p->flat_v, ent_cap, c0);                      \
+            if (zr) LAUNCH_Q2(R, CC, true); else LAUNCH_Q2(R, CC, false);                                      \
         } while (0)
         switch (p->proj_rpt * 100 + Cq) {
             case 108: LAUNCH_Q(1, 8); break;
+            case 112: LAUNCH_Q(1, 12); break;
             case 116: LAUNCH_Q(1, 16); break;
             case 132: LAUNCH_Q(1, 32); break;
             case 208: LAUNCH_Q(2, 8); break;
+            case 212: LAUNCH_Q(2, 12); break;
             case 216: LAUNCH_Q(2, 16); break;
             case 232: LAUNCH_Q(2, 32); break;
             case 408: LAUNCH_Q(4, 8); break;
+            case 412: LAUNCH_Q(4, 12); break;
             case 416: LAUNCH_Q(4, 16); break;
             default: LAUNCH_Q(4, 32); break;
         }
 #undef LAUNCH_Q
+#undef LAUNCH_Q2
         CBCT_CHECK(cudaGetLastError());
         cbct_count_launch();
         return 0;
