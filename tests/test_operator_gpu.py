@@ -127,6 +127,16 @@ def _check_random(op, ref):
     assert max_rel(got, want) <= TOL, max_rel(got, want)
 
 
+def test_flat_row_closed_form_against_oracle():
+    """Odd detector height puts a row exactly at the source height (the reference's flat
+    ray, operator.py:87-89): the boundary backprojector's FLAT variant with the closed-form
+    straddle, at config-2 cell sizes."""
+    vg, tr = baseline_geometry(256, 360, 512, 383, views=(40, 3))
+    op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    assert op.info.bp_fast_path == 1 and op.info.bp_closed_form == 1
+    _check_random(op, ref)
+
+
 def test_config3_views_against_oracle():
     """BASELINE config 3 (512^3, 720 views, 616x480) on two views: the prefix-sum projector
     at zs = 520 and the closed-form boundary backprojector at 0.43 mm voxels."""
