@@ -272,6 +272,22 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Block -> detector column, in tiles of kTileV views x kTileU columns (a bijection onto the
+// (view1 - view0) * nu columns of the launch).  The columns of a tile cross one ~40 mm strip of
+// the volume, so the CTAs in flight re-read the same cell columns from L2 instead of streaming
+// the whole volume once per view from DRAM (config 3: 537 MB volume > 126 MB L2).
+constexpr int kTileV = 8, kTileU = 64;
+__device__ __forceinline__ int64_t tiled_column(int b, int view0, int nviews, int nu) {
+    const int band = b / (kTileV * nu);               // band of kTileV views
+    const int vb = min(kTileV, nviews - band * kTileV);
+    const int r = b - band * kTileV * nu;             // index inside the band: [0, vb * nu)
+    const int ut = r / (vb * kTileU);                 // column tile
+    const int ub = min(kTileU, nu - ut * kTileU);
+    const int rem = r - ut * vb * kTileU;             // [0, vb * ub)
+    const int dv = rem / ub, du = rem - dv * ub;      // adjacent columns of one view run together
+    return (int64_t)(view0 + band * kTileV + dv) * nu + ut * kTileU + du;
+}
+
 // Guard-padded slab range [x, y] that some ray of a column can occupy while tau is in
 // [tau_a, tau_b]: z = w t is extremal at the corners of [w_lo, w_hi] x [t_a, t_b]; one slab of
 // margin on each side absorbs rounding.  Producer and consumers evaluate it identically.
@@ -292,7 +308,8 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                                                    const float2* __restrict__ col_ent, const double* __restrict__ wtab,
                                                    const float* __restrict__ vol, float* __restrict__ proj,
                                                    double* __restrict__ partials, int nv, int nz, int zs, double lo2,
-                                                   double p2, int flat_v, int ent_cap, int64_t c0) {
+                                                   double p2, int flat_v, int ent_cap, int64_t c0, int nu,
+                                                   int nviews) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
     uint64_t* empty = full + 2;                               // [2]
@@ -313,7 +330,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     const bool producer = warp == nwc;
     const int slot_elems = (C + RZ) * zs;
 
-    const int64_t c = c0 + blockIdx.x;  // detector column (view * nu + u)
+    const int64_t c = tiled_column((int)blockIdx.x, (int)(c0 / nu), nviews, nu);  // detector column (view * nu + u)
     const ColumnHeader h = cols[c];
     const int64_t off = col_off[c];
     const int M = (int)(col_off[c + 1] - off);
@@ -470,7 +487,8 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
                                             (int)smem));                                                       \
             k_project_q<R, CC, Z><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol,    \
                                                          proj, partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
-                                                         p->lo[2], p->pitch[2], p->flat_v, ent_cap, c0);        \
+                                                         p->lo[2], p->pitch[2], p->flat_v, ent_cap, c0,         \
+                                                         (int)p->nu, (int)(view1 - view0));                     \
         } while (0)
 #define LAUNCH_Q(R, CC)                                                                                        \
         do {                                                                                                   \
