@@ -199,6 +199,7 @@ def run_reference(args, cfg, rank, world):
 
 # ------------------------------------------------------------------ GPU leg --
 def run_ours(args, cfg, rank, world, local_rank):
+    """N = 1: the single-GPU CGLS step (N > 1 goes through run_sharded)."""
     import torch
 
     import paper_2110_13526_b200 as P
@@ -240,8 +241,6 @@ def run_ours(args, cfg, rank, world, local_rank):
     for _ in range(warmup):
         run.step(record=False)
     chain.apply, chain.applyT = timed("A", orig_apply), timed("AT", orig_applyT)
-    if world > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.lib().cbct_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -273,10 +272,6 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     t_a = kernel_ms(lambda: op.project_internal(run.d, run.p))
     t_at = kernel_ms(lambda: op.backproject_internal(run.e, run.r, scratch=scratch))
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / steps
     value = 1e3 / ms_step
 
@@ -473,12 +468,7 @@ def main():
         rc = run_sharded(args, args.config, rank, world, local_rank)
         torch.distributed.destroy_process_group()
         return rc
-    rc = run_ours(args, args.config, rank, world, local_rank)
-    if world > 1:
-        import torch
-
-        torch.distributed.destroy_process_group()
-    return rc
+    return run_ours(args, args.config, rank, world, local_rank)
 
 
 if __name__ == "__main__":
