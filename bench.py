@@ -464,7 +464,7 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29531")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         rc = run_sharded(args, args.config, rank, world, local_rank)
         torch.distributed.destroy_process_group()
         return rc
