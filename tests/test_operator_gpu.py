@@ -137,6 +137,19 @@ def test_flat_row_closed_form_against_oracle():
     _check_random(op, ref)
 
 
+def test_principal_point_offset_closed_form_against_oracle():
+    """A principal-point offset moves the detector centre c0 off the half-integer grid, so the
+    closed-form backprojector's split c0 = c0i + c0f carries an arbitrary fraction."""
+    import paper_2110_13526_b200 as P
+
+    vg, tr0 = baseline_geometry(256, 360, 512, 384, views=(200, 3))
+    det = P.DetectorGeometry(512, 384, tr0.detector.pixel_size, (0.37, -1.13))
+    tr = P.make_circular_trajectory(tr0.sid, tr0.sdd, tr0.n_views, tr0.start_angle, tr0.angular_span, det)
+    op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    assert op.info.bp_fast_path == 1 and op.info.bp_closed_form == 1
+    _check_random(op, ref)
+
+
 def test_config3_views_against_oracle():
     """BASELINE config 3 (512^3, 720 views, 616x480) on two views: the prefix-sum projector
     at zs = 520 and the closed-form boundary backprojector at 0.43 mm voxels."""
