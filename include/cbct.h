@@ -150,6 +150,21 @@ int cbct_axpby(int64_t n, double a, const float* x, double b, float* y, double* 
 int cbct_sub(int64_t n, const float* a, const float* b, float* out, double* partials, void* stream);
 /* partials of x . y */
 int cbct_dot(int64_t n, const float* x, const float* y, double* partials, void* stream);
+/* Device-resident CGLS loop (no host round trip per iteration; CUDA-graph capturable).
+ * `scalars` is a device fp64 array: [0] ||r||^2 of the previous iteration, [1] ||r||^2
+ * (written by cbct_reduce_partials after A^T), [2] ||p||^2 (after A), [3] alpha (the
+ * deferred x step), [4] beta, [5] ||e||^2 (after the e update), [6] state (0 running,
+ * 1 breakdown, 2 converged to [9]), [7] iterations done, [8] ||b||, [9] relative
+ * discrepancy tolerance, [10] x-update flag, [16 + i] ||e||^2 of iteration i.
+ * cbct_cgls_scalars evaluates the host loop's recurrences (solvers.py:339-357) in the
+ * same fp64 operations -- stage 1 after A^T (beta), 2 after A (alpha), 3 after the e
+ * update (history, tolerance) -- so the iterates are bitwise those of the host loop.
+ * The two updates read their scalars from the array and are no-ops once state != 0. */
+int cbct_cgls_scalars(double* scalars, int stage, void* stream);
+int cbct_cgls_volume_update_dev(int64_t n, float* x, float* d, const float* r, const double* scalars,
+                                void* stream);
+int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, const double* scalars, double* partials,
+                              void* stream);
 /* Deterministic fixed-order sum of n fp64 partials into *dev_out; if host_out is
  * not NULL the result is also copied there (synchronising the stream). */
 int cbct_reduce_partials(const double* partials, int32_t n, double* dev_out, double* host_out, void* stream);

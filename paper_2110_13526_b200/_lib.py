@@ -71,6 +71,9 @@ SIGNATURES = {
     "cbct_fill": (c_i32, [c_i64, c_p, c_f32, c_p]),
     "cbct_fill_volume": (c_i32, [c_p, c_p, c_f32, c_p]),
     "cbct_phantom": (c_i32, [c_p, c_p, c_i32, c_p, c_p]),
+    "cbct_cgls_scalars": (c_i32, [c_p, c_i32, c_p]),
+    "cbct_cgls_volume_update_dev": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_cgls_proj_update_dev": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "cbct_phantom_ref": (c_i32, [c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p]),
     "cbct_ref_project": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,
                                  c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64, c_i64, c_i64]),

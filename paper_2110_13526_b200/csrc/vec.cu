@@ -141,6 +141,98 @@ __global__ void k_reduce(const double* __restrict__ partials, int n, double* __r
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// ---------------------------------------------------------------------------
+// Device-resident CGLS scalars (the host loop's recurrences, solvers.py:339-357, in the same
+// fp64 operations, so results are bitwise identical to it).  Layout of S (include/cbct.h):
+enum : int {
+    kSNr2Old = 0, kSNr2 = 1, kSNp2 = 2, kSAlpha = 3, kSBeta = 4, kSNb2 = 5, kSState = 6, kSIter = 7, kSNb0 = 8,
+    kSTol = 9, kSDoX = 10, kSHist = 16
+};
+
+__global__ void k_cgls_scalars(double* __restrict__ S, int stage) {
+    if (S[kSState] != 0.0) return;  // stopped: every later stage and vector update is a no-op
+    if (stage == 1) {               // after A^T: ||r||^2 in S[kSNr2]
+        const double nr2 = S[kSNr2];
+        if (nr2 == 0.0) {
+            S[kSState] = 1.0;  // breakdown (the deferred x update stays pending)
+            return;
+        }
+        S[kSBeta] = nr2 / S[kSNr2Old];
+        S[kSDoX] = S[kSAlpha] != 0.0 ? 1.0 : 0.0;
+        S[kSNr2Old] = nr2;
+    } else if (stage == 2) {  // after A: ||p||^2 in S[kSNp2]
+        const double np2 = S[kSNp2];
+        if (np2 == 0.0) {
+            S[kSState] = 1.0;
+            S[kSAlpha] = 0.0;  // the update already consumed the pending alpha
+            return;
+        }
+        S[kSAlpha] = S[kSNr2Old] / np2;
+    } else {  // after e -= alpha p: ||e||^2 in S[kSNb2]
+        const double it = S[kSIter] + 1.0;
+        S[kSIter] = it;
+        S[kSHist + (int)it] = S[kSNb2];
+        const double nb0 = S[kSNb0];
+        const double rel = nb0 > 0.0 ? sqrt(S[kSNb2]) / nb0 : 0.0;
+        if (!(rel > S[kSTol])) S[kSState] = 2.0;  // converged to the tolerance
+    }
+}
+
+__global__ void k_cgls_volume_dev(int64_t n, float* __restrict__ x, float* __restrict__ d,
+                                  const float* __restrict__ r, const double* __restrict__ S, int use4) {
+    if (S[kSState] != 0.0) return;
+    const float alpha_prev = (float)S[kSAlpha], beta = (float)S[kSBeta];
+    const int do_x = S[kSDoX] != 0.0;
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* d4 = reinterpret_cast<float4*>(d);
+    const float4* r4 = reinterpret_cast<const float4*>(r);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 dv = d4[i];
+        const float4 rv = r4[i];
+        if (do_x) {
+            float4 xv = x4[i];
+            xv.x = fmaf(alpha_prev, dv.x, xv.x); xv.y = fmaf(alpha_prev, dv.y, xv.y);
+            xv.z = fmaf(alpha_prev, dv.z, xv.z); xv.w = fmaf(alpha_prev, dv.w, xv.w);
+            x4[i] = xv;
+        }
+        dv.x = fmaf(beta, dv.x, rv.x); dv.y = fmaf(beta, dv.y, rv.y);
+        dv.z = fmaf(beta, dv.z, rv.z); dv.w = fmaf(beta, dv.w, rv.w);
+        d4[i] = dv;
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (do_x) x[i] = fmaf(alpha_prev, d[i], x[i]);
+        d[i] = fmaf(beta, d[i], r[i]);
+    }
+}
+
+// e -= alpha p with alpha = S[kSAlpha]; partials of e^2 (same arithmetic as k_axpby(-alpha, p, 1, e))
+__global__ void k_cgls_proj_dev(int64_t n, float* __restrict__ e, const float* __restrict__ p,
+                                const double* __restrict__ S, double* __restrict__ partials, int use4) {
+    if (S[kSState] != 0.0) return;
+    const float a = (float)(-S[kSAlpha]), b = 1.0f;
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    float4* e4 = reinterpret_cast<float4*>(e);
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 yv = e4[i];
+        const float4 xv = p4[i];
+        yv.x = fmaf(a, xv.x, b * yv.x); yv.y = fmaf(a, xv.y, b * yv.y);
+        yv.z = fmaf(a, xv.z, b * yv.z); yv.w = fmaf(a, xv.w, b * yv.w);
+        e4[i] = yv;
+        sq += (double)yv.x * yv.x + (double)yv.y * yv.y + (double)yv.z * yv.z + (double)yv.w * yv.w;
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float yv = fmaf(a, p[i], b * e[i]);
+        e[i] = yv;
+        sq += (double)yv * yv;
+    }
+    finish(sq, partials);
+}
+
 }  // namespace
 
 extern "C" int cbct_vec_blocks(int64_t n) { return vec_blocks(n); }
@@ -232,5 +324,33 @@ extern "C" int cbct_reduce_partials(const double* partials, int32_t n, double* d
         CBCT_CHECK(cudaMemcpyAsync(host_out, dev_out, sizeof(double), cudaMemcpyDeviceToHost, s));
         CBCT_CHECK(cudaStreamSynchronize(s));
     }
+    return 0;
+}
+
+extern "C" int cbct_cgls_scalars(double* scalars, int stage, void* stream) {
+    if (!scalars || stage < 1 || stage > 3) return cbct_fail(CBCT_E_ARG, "cbct_cgls_scalars: bad argument");
+    k_cgls_scalars<<<1, 1, 0, (cudaStream_t)stream>>>(scalars, stage);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_cgls_volume_update_dev(int64_t n, float* x, float* d, const float* r, const double* scalars,
+                                           void* stream) {
+    if (!x || !d || !r || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_cgls_volume_update_dev: null argument");
+    const int use4 = aligned16(x) && aligned16(d) && aligned16(r);
+    k_cgls_volume_dev<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, d, r, scalars, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, const double* scalars,
+                                         double* partials, void* stream) {
+    if (!e || !p || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_cgls_proj_update_dev: null argument");
+    const int use4 = aligned16(e) && aligned16(p);
+    k_cgls_proj_dev<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, e, p, scalars, partials, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
     return 0;
 }

@@ -220,20 +220,31 @@ class CbctOperator:
         return t, t.dtype == torch.float64
 
     # ------------------------------------------------------- device kernels --
-    def project_internal(self, x: torch.Tensor, out: torch.Tensor, norm2: bool = False):
-        """out = A x on device layouts; returns ||out||^2 (fp64, deterministic) if norm2."""
-        part = self._partials if norm2 else None
+    def project_internal(self, x: torch.Tensor, out: torch.Tensor, norm2: bool = False, norm_out=None):
+        """out = A x on device layouts; returns ||out||^2 (fp64, deterministic) if norm2.
+        With ``norm_out`` (a 1-element fp64 device tensor) the norm is reduced into it on the
+        device instead, with no host round trip (device-resident solver loops)."""
+        part = self._partials if (norm2 or norm_out is not None) else None
         call("cbct_project", self._plan, _ptr(x), _ptr(out), _ptr(part), self._stream())
+        if norm_out is not None:
+            return self.reduce_to(int(self.info.proj_blocks), norm_out)
         return self.reduce(int(self.info.proj_blocks)) if norm2 else None
 
     def backproject_internal(self, y, out: torch.Tensor, mode: int = 1, norm2: bool = False, col_scale=None,
-                             scratch=None):
-        """out = A^T y (mode 1) or diag(A^T A) (mode 2, y ignored); ||out||^2 if norm2."""
+                             scratch=None, norm_out=None):
+        """out = A^T y (mode 1) or diag(A^T A) (mode 2, y ignored); ||out||^2 if norm2 (or, with
+        ``norm_out``, reduced on the device into that 1-element fp64 tensor)."""
         scratch = self.new_bp_scratch() if scratch is None else scratch
-        part = self._partials if norm2 else None
+        part = self._partials if (norm2 or norm_out is not None) else None
         call("cbct_backproject", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode), _ptr(scratch),
              _ptr(col_scale), _ptr(part), self._stream())
+        if norm_out is not None:
+            return self.reduce_to(int(self.info.bp_blocks), norm_out)
         return self.reduce(int(self.info.bp_blocks)) if norm2 else None
+
+    def reduce_to(self, n_partials: int, out: torch.Tensor) -> None:
+        """Deterministic sum of the first n partials into the fp64 device scalar ``out`` (no sync)."""
+        call("cbct_reduce_partials", _ptr(self._partials), int(n_partials), _ptr(out), None, self._stream())
 
     def reduce(self, n_partials: int) -> float:
         """Deterministic sum of the first n partials (synchronises the stream)."""

@@ -469,6 +469,78 @@ class CglsRun:
             self._record(self.i)
         return True
 
+    # ------------------------------------------------- device-resident iterations --
+    def device_capable(self) -> bool:
+        """The plain fused chain (no Jacobi/Tikhonov stacking) without true-discrepancy
+        monitoring can run with every scalar on the device (``run_device``)."""
+        c = self.chain
+        return type(c) is _Chain and c._fused and self.cfg.true_discrepancy_every <= 0
+
+    def _device_scalars(self) -> torch.Tensor:
+        """The fp64 scalar array of include/cbct.h cbct_cgls_scalars, loaded from the host state."""
+        if getattr(self, "_S", None) is None:
+            self._S = torch.zeros(16 + self.cfg.max_iterations + 2, dtype=torch.float64, device=self.dev.device)
+        host = torch.tensor([self.nr2_old, 0.0, 0.0, self.pending, 0.0, 0.0, 0.0, float(self.i), self.nb0,
+                             float(self.cfg.rel_discrepancy_tol), 0.0], dtype=torch.float64)
+        self._S[:11].copy_(host)
+        return self._S
+
+    def _device_iteration(self, S):
+        op, dev, st = self.op, self.dev, self.dev.s
+        op.backproject_internal(self.e, self.r, scratch=self.chain._scratch(), norm_out=S[1:2])
+        call("cbct_cgls_scalars", _p(S), 1, st())                                   # beta
+        call("cbct_cgls_volume_update_dev", self.d.numel(), _p(self.x), _p(self.d), _p(self.r), _p(S), st())
+        op.project_internal(self.d, self.p, norm_out=S[2:3])
+        call("cbct_cgls_scalars", _p(S), 2, st())                                   # alpha
+        call("cbct_cgls_proj_update_dev", self.e.numel(), _p(self.e), _p(self.p), _p(S), _p(dev.partials), st())
+        op.reduce_to(dev.nblocks(self.e.numel()), S[5:6])
+        call("cbct_cgls_scalars", _p(S), 3, st())                                   # history, tolerance
+
+    def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
+        """Up to k loop iterations with alpha, beta, the norms and the stop tests on the device
+        (csrc/vec.cu cbct_cgls_scalars): no host round trip inside, one synchronisation at the end,
+        and iterates bit-identical to k calls of ``step``.  Iterations after a breakdown or after
+        reaching the tolerance are no-ops for the iterate.  ``graph`` replays one captured CUDA
+        graph of the iteration instead of issuing its launches from Python (``graph_launches`` is
+        then the number of kernels per replay).  ``collect=False`` leaves the batch in flight;
+        ``collect()`` synchronises and reads the history back.  History records of a batch share
+        its end time."""
+        if self.done or k <= 0:
+            return
+        S = self._device_scalars()
+        self._i0 = self.i
+        if graph:
+            if getattr(self, "_graph", None) is None:
+                from ._lib import lib
+
+                self.chain._scratch()
+                g = torch.cuda.CUDAGraph()
+                n0 = lib().cbct_launch_count()
+                with torch.cuda.graph(g):
+                    self._device_iteration(S)
+                self.graph_launches = lib().cbct_launch_count() - n0
+                self._graph = g
+            for _ in range(k):
+                self._graph.replay()
+        else:
+            for _ in range(k):
+                self._device_iteration(S)
+        if collect:
+            self.collect()
+
+    def collect(self) -> None:
+        """Synchronise with the device loop and fold its scalars and history into the host state."""
+        h = self._S.cpu().numpy()
+        self.nr2_old, self.pending = float(h[0]), float(h[3])
+        it = int(h[7])
+        now = time.perf_counter() - self.t0
+        for j in range(self._i0 + 1, it + 1):
+            self.nb = float(np.sqrt(h[16 + j]))
+            self.history.append(ConvergenceRecord(j, now, self.rel(self.nb), None))
+        self.i = it
+        if h[6] == 1.0:
+            self.done = self.breakdown = True
+
     def report(self) -> SolverReport:
         self.flush()
         op = self.op
@@ -480,10 +552,18 @@ def cgls(op, b, cfg: SolverConfig) -> SolverReport:
     """CGLS with delayed residual (solvers.py:269-358): K+2 A, K+1 A^T."""
     _check_inputs(op, b, cfg, "cgls")
     run = CglsRun(op, b, cfg)
+    if run.device_capable():
+        # batches of device-resident iterations (one host synchronisation per batch)
+        while run.should_continue():
+            run.run_device(min(_DEVICE_BATCH, cfg.max_iterations - run.i))
+        return run.report()
     while run.should_continue():
         if not run.step():
             break
     return run.report()
+
+
+_DEVICE_BATCH = 8
 
 
 def _proj_update(dev, chain, e, p, alpha):

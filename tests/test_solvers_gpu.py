@@ -302,3 +302,32 @@ def test_device_tensor_inputs_stay_on_device(small):
     assert isinstance(rep.final_x.data, torch.Tensor) and rep.final_x.data.is_cuda
     host = S.cgls(op, P.ProjectionStack(op.trajectory, d["solver_b"].astype(np.float32)), cfg)
     np.testing.assert_array_equal(rep.final_x.data.double().cpu().numpy(), host.final_x.data)
+
+
+def test_device_resident_cgls_loop_is_bitwise_the_host_loop():
+    """CglsRun.run_device (scalars, stop tests and history on the device, optional CUDA graph)
+    reproduces CglsRun.step exactly: same fp64 recurrences, same fp32 roundings."""
+    P, S = _mods()
+    d = load_golden("adjoint_instance")
+    vg, tr = geom_from_golden(d)
+    op = P.CbctOperator(vg, tr)
+    truth = P.generate_phantom(P.shepp_logan_3d(), vg)
+    b = op.project(truth)
+    for tol, K, batches in ((0.0, 12, (5, 7)), (0.2, 30, (8, 8, 8, 8))):
+        cfg = S.SolverConfig(method="cgls", max_iterations=K, rel_discrepancy_tol=tol)
+        host = S.CglsRun(op, b, cfg)
+        while host.should_continue():
+            if not host.step():
+                break
+        for graph in (False, True):
+            dev = S.CglsRun(op, b, cfg)
+            assert dev.device_capable()
+            for k in batches:
+                if dev.should_continue():
+                    dev.run_device(min(k, K - dev.i), graph=graph)
+            assert dev.i == host.i and dev.breakdown == host.breakdown
+            assert [r.rel_discrepancy for r in dev.history] == [r.rel_discrepancy for r in host.history]
+            assert dev.pending == host.pending and dev.nr2_old == host.nr2_old
+            assert torch.equal(dev.x, host.x) and torch.equal(dev.d, host.d) and torch.equal(dev.e, host.e)
+    rep = S.cgls(op, b, S.SolverConfig(method="cgls", max_iterations=9))  # the public driver (device loop)
+    assert rep.iterations == 9 and len(rep.history) == 10
