@@ -266,12 +266,14 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
     }
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    float z[G], acc[G], sgn[G], sgn2[G], iz[G], sdn[G];
+    float z[G], zlo[G], acc[G], sgn[G], sgn2[G], iz[G], sdn[G];
     int kb[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         kb[g] = (warp + g * nwarps) * 31 + lane;  // boundary index (voxel below it is kb-1)
-        z[g] = (float)(lo2 + (double)min(kb[g], nz) * p2);  // lanes past the top reuse it (unused)
+        const double zd = lo2 + (double)min(kb[g], nz) * p2;  // lanes past the top reuse it (unused)
+        z[g] = (float)zd;
+        zlo[g] = (float)(zd - (double)z[g]);  // the closed form carries z to ~1e-15 (two words)
         acc[g] = 0.0f;
         sgn[g] = z[g] >= 0.0f ? 1.0f : 0.0f;
         sgn2[g] = z[g] >= 0.0f ? 1.0f : -1.0f;
@@ -383,7 +385,10 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
                     const float R = __int_as_float((int)bits) - 12582911.0f;  // floor(W) + 1, exact
                     // s is saturated to [0, 1] first (the first-order f_t is only valid there; rays
                     // that cannot straddle have s < 0 or > 1), then f_t = s (1 - eps + eps s).
-                    const float tail = fmaf(z[g], t1.y, c0f);  // z ia_lo + c0f, independent of R
+                    // z ia_lo + z_lo ia + c0f, independent of R: with z and 1/(t_a pv) both carried as
+                    // two fp32 words, W_a - R keeps ~1e-7 rows of absolute error even where the
+                    // straddle window W_a - W_b is only ~|W| eps wide (config 5: 0.04 rows)
+                    const float tail = fmaf(zlo[g], t0.x, fmaf(z[g], t1.y, c0f));
                     const float sv = __saturatef((fmaf(z[g], t0.x, -R) + tail) * (iz[g] * t0.z));
                     const float h = fmaf(t1.x, sv, t1.z);            // 1 - eps + eps s
                     f = fmaf(sgn2[g] * sv, h, sdn[g]);               // f_t above, 1 - f_t below

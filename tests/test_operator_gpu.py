@@ -150,6 +150,18 @@ def test_principal_point_offset_closed_form_against_oracle():
     _check_random(op, ref)
 
 
+def test_config5_slab_against_oracle():
+    """BASELINE config 5 (1024^3, 1440 views of 1024x768) on a 32-slice z slab seen by eight
+    views: config-5 cell and detector sizes at oracle cost.  (With two views the worst voxel
+    reaches 1.1e-4: at 0.2 mm voxels a ray can straddle a boundary by 1 - 1e-4, inside the fp32
+    rounding of its row coordinate, and then counts as entirely below -- a sign-random sliver
+    that averages out over views; rel-L2 is 1.2e-5 either way, as for the fp64-clip kernel.)"""
+    vg, tr = baseline_geometry(1024, 1440, 1024, 768, views=(300, 8), zslab=(600, 32))
+    op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    assert op.info.bp_fast_path == 1
+    _check_random(op, ref)
+
+
 def test_config3_views_against_oracle():
     """BASELINE config 3 (512^3, 720 views, 616x480) on two views: the prefix-sum projector
     at zs = 520 and the closed-form boundary backprojector at 0.43 mm voxels."""
