@@ -187,6 +187,9 @@ int cbct_fill_volume(const cbct_plan* plan, float* vol, float value, void* strea
 int cbct_phantom(const cbct_plan* plan, const double* ellipsoids, int n_ell, float* vol, void* stream);
 int cbct_phantom_ref(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, float* out,
                      void* stream);
+/* Same sums without the final rounding: fp64, bit-identical to the host generator for any table. */
+int cbct_phantom_ref_f64(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, double* out,
+                         void* stream);
 
 /* ---- reference-signature entry points (host fp64, reference layouts) ------ */
 /* Drop-in for _project_kernel (operator.py:190-206). */

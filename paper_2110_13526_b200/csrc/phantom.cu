@@ -56,15 +56,16 @@ __global__ void k_phantom_internal(const double* __restrict__ ell, int n_ell, in
     }
 }
 
-// reference layout (nz, ny, nx), x fastest (phantom.py:72-75)
+// reference layout (nz, ny, nx), x fastest (phantom.py:72-75); T = float or double
+template <typename T>
 __global__ void k_phantom_ref(const double* __restrict__ ell, int n_ell, int nx, int ny, int nz,
-                              float* __restrict__ out) {
+                              T* __restrict__ out) {
     const int64_t total = (int64_t)nz * ny * nx;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int ix = (int)(i % nx);
         const int64_t r = i / nx;
         const int iy = (int)(r % ny), iz = (int)(r / ny);
-        out[i] = (float)ellipsoid_sum(ell, n_ell, axis_centre(ix, nx), axis_centre(iy, ny), axis_centre(iz, nz));
+        out[i] = (T)ellipsoid_sum(ell, n_ell, axis_centre(ix, nx), axis_centre(iy, ny), axis_centre(iz, nz));
     }
 }
 
@@ -86,15 +87,25 @@ extern "C" int cbct_phantom(const cbct_plan* p, const double* ellipsoids, int n_
     return 0;
 }
 
-extern "C" int cbct_phantom_ref(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, float* out,
-                                void* stream) {
+template <typename T>
+int phantom_ref(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, T* out, void* stream) {
     if (nx <= 0 || ny <= 0 || nz <= 0 || nx > INT32_MAX || ny > INT32_MAX || nz > INT32_MAX)
         return cbct_fail(CBCT_E_ARG, "cbct_phantom_ref: bad dimensions");
     if (!out || (n_ell > 0 && !ellipsoids) || n_ell < 0)
         return cbct_fail(CBCT_E_ARG, "cbct_phantom_ref: null argument or negative count");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    k_phantom_ref<<<grid_for(nx * ny * nz), 256, 0, s>>>(ellipsoids, n_ell, (int)nx, (int)ny, (int)nz, out);
+    k_phantom_ref<T><<<grid_for(nx * ny * nz), 256, 0, s>>>(ellipsoids, n_ell, (int)nx, (int)ny, (int)nz, out);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch(1);
     return 0;
+}
+
+extern "C" int cbct_phantom_ref(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell, float* out,
+                                void* stream) {
+    return phantom_ref<float>(nx, ny, nz, ellipsoids, n_ell, out, stream);
+}
+
+extern "C" int cbct_phantom_ref_f64(int64_t nx, int64_t ny, int64_t nz, const double* ellipsoids, int n_ell,
+                                    double* out, void* stream) {
+    return phantom_ref<double>(nx, ny, nz, ellipsoids, n_ell, out, stream);
 }
