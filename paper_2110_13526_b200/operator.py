@@ -145,6 +145,11 @@ class CbctOperator:
         # sklearn.clone deep-copies estimators (test_estimators.py:35-43): rebuild the plan.
         return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device)
 
+    def __reduce__(self):
+        # pickling (joblib workers of sklearn model selection) carries the geometry; the device
+        # plan is rebuilt on load
+        return (CbctOperator, (self.vol_geom, self.trajectory, self.workers, str(self.device)))
+
     # ------------------------------------------------------------ properties --
     @property
     def n(self) -> int:
