@@ -344,18 +344,19 @@ def run_sharded(args, cfg, rank, world, local_rank):
     steps, warmup = args.steps, args.warmup
     run = DistCglsRun(sop, vec, b_local, SolverConfig(method="cgls", max_iterations=steps + warmup + 1), record=False)
     stream = torch.cuda.current_stream(dev)
-    for _ in range(warmup):
-        run.step()
+    # device-resident sharded loop: norm partials all-gathered and summed on the GPU, no host
+    # round trip inside the K iterations (distributed.DistCglsRun.run_device)
+    run.run_device(warmup)
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.lib().cbct_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         start.record(stream)
-        for _ in range(steps):
-            run.step()
+        run.run_device(steps)
         end.record(stream)
         torch.cuda.synchronize()
+    assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
     launches = _lib.lib().cbct_launch_count() - launches0
     t = torch.tensor([start.elapsed_time(end)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -386,7 +387,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
     bl = b_host.to(dev, non_blocking=True)
     r2 = DistCglsRun(sop, vec, bl, SolverConfig(method="cgls", max_iterations=e2e_k), record=False)
     while r2.should_continue():
-        r2.step()
+        r2.run_device(e2e_k - r2.i)
     _, x_loc = r2.finish()
     x_full = sop.gather_volume(x_loc)
     x_host = x_full[: op.vol_elems].cpu() if rank == 0 else None

@@ -165,6 +165,9 @@ int cbct_cgls_volume_update_dev(int64_t n, float* x, float* d, const float* r, c
                                 void* stream);
 int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, const double* scalars, double* partials,
                               void* stream);
+/* Multi-GPU: *out = vals[0] + vals[1] + ... in index order (the per-rank norm partials after an
+ * all_gather), the same fp64 additions as the host's rank-ordered sum. */
+int cbct_sum_ranks(const double* vals, int n, double* out, void* stream);
 /* Deterministic fixed-order sum of n fp64 partials into *dev_out; if host_out is
  * not NULL the result is also copied there (synchronising the stream). */
 int cbct_reduce_partials(const double* partials, int32_t n, double* dev_out, double* host_out, void* stream);

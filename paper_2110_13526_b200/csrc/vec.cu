@@ -178,6 +178,13 @@ __global__ void k_cgls_scalars(double* __restrict__ S, int stage) {
     }
 }
 
+// sum of n per-rank values in index (rank) order: the host loop's `acc += v` sequence, on device
+__global__ void k_sum_ranks(const double* __restrict__ vals, int n, double* __restrict__ out) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += vals[i];
+    *out = acc;
+}
+
 __global__ void k_cgls_volume_dev(int64_t n, float* __restrict__ x, float* __restrict__ d,
                                   const float* __restrict__ r, const double* __restrict__ S, int use4) {
     if (S[kSState] != 0.0) return;
@@ -350,6 +357,14 @@ extern "C" int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, co
     if (!e || !p || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_cgls_proj_update_dev: null argument");
     const int use4 = aligned16(e) && aligned16(p);
     k_cgls_proj_dev<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, e, p, scalars, partials, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_sum_ranks(const double* vals, int n, double* out, void* stream) {
+    if (!vals || !out || n < 1) return cbct_fail(CBCT_E_ARG, "cbct_sum_ranks: bad argument");
+    k_sum_ranks<<<1, 1, 0, (cudaStream_t)stream>>>(vals, n, out);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();
     return 0;

@@ -121,7 +121,10 @@ class ShardedOperator:
     def _p(self, t):
         return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
-    def _reduce(self, n):
+    def _reduce(self, n, norm_out=None):
+        if norm_out is not None:  # device scalar, no host round trip
+            call("cbct_reduce_partials", self._p(self._parts), int(n), self._p(norm_out), None, self._s())
+            return None
         call("cbct_reduce_partials", self._p(self._parts), int(n), self._p(self.op._red),
              ctypes.byref(self.op._host), self._s())
         return float(self.op._host.value)
@@ -132,23 +135,31 @@ class ShardedOperator:
     def gather_proj(self, local):
         return self.comm.all_gather(local, self._e_full)
 
-    def project_local(self, d_full, p_local, norm2=False):
-        """p_local = (A d)[views v0..v1) ; returns the local ||p||^2 partial."""
+    def project_local(self, d_full, p_local, norm2=False, norm_out=None):
+        """p_local = (A d)[views v0..v1) ; returns the local ||p||^2 partial (or reduces it into the
+        device scalar ``norm_out``)."""
         if self.v1 <= self.v0:
+            if norm_out is not None:
+                norm_out.zero_()
             return 0.0 if norm2 else None
         n = (self.v1 - self.v0) * self.nu
+        want = norm2 or norm_out is not None
         call("cbct_project_views", self.op._plan, self._p(d_full), self._p(p_local), self.v0, self.v1,
-             self._p(self._parts) if norm2 else None, self._s())
-        return self._reduce(n) if norm2 else None
+             self._p(self._parts) if want else None, self._s())
+        return self._reduce(n, norm_out) if want else None
 
-    def backproject_local(self, e_full, r_local, norm2=False):
-        """r_local = (A^T e)[cell rows y0..y1) ; returns the local ||r||^2 partial."""
+    def backproject_local(self, e_full, r_local, norm2=False, norm_out=None):
+        """r_local = (A^T e)[cell rows y0..y1) ; returns the local ||r||^2 partial (or reduces it into
+        the device scalar ``norm_out``)."""
         if self.y1 <= self.y0:
+            if norm_out is not None:
+                norm_out.zero_()
             return 0.0 if norm2 else None
         n = -(-self.nx // 16) * -(-(self.y1 - self.y0) // 16) * 256
+        want = norm2 or norm_out is not None
         call("cbct_backproject_rows", self.op._plan, self._p(e_full), self._p(r_local), self.y0, self.y1, 1,
-             self._p(self._scratch), None, self._p(self._parts) if norm2 else None, self._s())
-        return self._reduce(n) if norm2 else None
+             self._p(self._scratch), None, self._p(self._parts) if want else None, self._s())
+        return self._reduce(n, norm_out) if want else None
 
 
 class DistCglsRun:
@@ -221,6 +232,60 @@ class DistCglsRun:
         self.i += 1
         self._rec(self.i)
         return True
+
+    # ------------------------------------------------- device-resident iterations --
+    def run_device(self, k: int) -> None:
+        """Up to k iterations with every scalar on the device (NCCL + libcbct only): the local norm
+        partials are reduced into device scalars, all-gathered (8 bytes per rank) and summed in rank
+        order by cbct_sum_ranks -- the same fp64 additions as ``TorchComm.allsum`` -- and
+        cbct_cgls_scalars / the device-scalar updates run the recurrences as in the single-GPU loop
+        (solvers.CglsRun.run_device).  One synchronisation at the end; iterates bit-identical to k
+        calls of ``step``."""
+        if self.done or k <= 0:
+            return
+        import torch
+
+        from ._lib import call as _call
+
+        sop, vec, dev = self.sop, self.vec, self.b.device
+        if getattr(self, "_S", None) is None:
+            self._S = torch.zeros(16 + self.cfg.max_iterations + 2, dtype=torch.float64, device=dev)
+            self._loc = torch.zeros(1, dtype=torch.float64, device=dev)
+            self._all = torch.zeros(sop.world, dtype=torch.float64, device=dev)
+        S, loc, allv = self._S, self._loc, self._all
+        S[:11].copy_(torch.tensor([self.nr2_old, 0.0, 0.0, self.pending, 0.0, 0.0, 0.0, float(self.i), self.nb0,
+                                   float(self.cfg.rel_discrepancy_tol), 0.0], dtype=torch.float64))
+        st = sop._s
+        p = sop._p
+
+        def allsum_into(slot):
+            sop.comm.all_gather(loc, allv)
+            _call("cbct_sum_ranks", p(allv), sop.world, p(S[slot:slot + 1]), st())
+
+        i0 = self.i
+        for _ in range(k):
+            sop.backproject_local(sop.gather_proj(self.e), self.r, norm_out=loc)
+            allsum_into(1)
+            _call("cbct_cgls_scalars", p(S), 1, st())
+            _call("cbct_cgls_volume_update_dev", self.d.numel(), p(self.x), p(self.d), p(self.r), p(S), st())
+            sop.project_local(sop.gather_volume(self.d), self.p, norm_out=loc)
+            allsum_into(2)
+            _call("cbct_cgls_scalars", p(S), 2, st())
+            _call("cbct_cgls_proj_update_dev", self.e.numel(), p(self.e), p(self.p), p(S),
+                  p(vec.dev.partials), st())
+            _call("cbct_reduce_partials", p(vec.dev.partials), vec.dev.nblocks(self.e.numel()), p(loc), None, st())
+            allsum_into(5)
+            _call("cbct_cgls_scalars", p(S), 3, st())
+        h = S.cpu().numpy()
+        self.nr2_old, self.pending = float(h[0]), float(h[3])
+        it = int(h[7])
+        for j in range(i0 + 1, it + 1):
+            self.nb = math.sqrt(h[16 + j])
+            self.i = j
+            self._rec(j)
+        self.i = it
+        if h[6] == 1.0:
+            self.done = self.breakdown = True
 
     def finish(self):
         if self.pending != 0.0:

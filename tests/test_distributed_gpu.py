@@ -87,3 +87,40 @@ def test_nccl_world1_driver_matches_cgls():
         assert np.linalg.norm(rep.final_x.data - xr) / np.linalg.norm(xr) <= 1e-5
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_world1_device_resident_loop_is_bitwise_the_host_loop():
+    """DistCglsRun.run_device (norm partials all-gathered on the device and summed in rank order by
+    cbct_sum_ranks, scalars and stop tests on the GPU) equals DistCglsRun.step exactly."""
+    import torch.distributed as dist
+
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200.distributed import CudaVectors, DistCglsRun, ShardedOperator, TorchComm
+    from paper_2110_13526_b200.solvers import SolverConfig
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        d = load_golden("adjoint_instance")
+        vg, tr = geom_from_golden(d)
+        sop = ShardedOperator(vg, tr, TorchComm())
+        b_int = sop.op.new_projections()
+        sop.op.project_internal(sop.op.phantom_internal(P.shepp_logan_3d()), b_int)
+        b_local = torch.zeros(sop.m_loc, device="cuda")
+        b_local[: b_int.numel()] = b_int
+        for tol, K in ((0.0, 9), (0.25, 30)):
+            cfg = SolverConfig(method="cgls", max_iterations=K, rel_discrepancy_tol=tol)
+            host = DistCglsRun(sop, CudaVectors(sop.op), b_local, cfg)
+            while host.should_continue():
+                if not host.step():
+                    break
+            devr = DistCglsRun(sop, CudaVectors(sop.op), b_local, cfg)
+            while devr.should_continue():
+                devr.run_device(min(4, K - devr.i))
+            assert devr.i == host.i and devr.pending == host.pending
+            assert [h.rel_discrepancy for h in devr.hist] == [h.rel_discrepancy for h in host.hist]
+            assert torch.equal(devr.x, host.x) and torch.equal(devr.d, host.d) and torch.equal(devr.e, host.e)
+    finally:
+        dist.destroy_process_group()
