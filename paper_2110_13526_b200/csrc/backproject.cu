@@ -433,7 +433,8 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode 1 needs projections");
     cudaStream_t s = (cudaStream_t)stream;
     const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
-    if (mode == 1 && p->bp_boundary_ok && !precise) {
+    static const bool force_direct = getenv("CBCT_BP_DIRECT") != nullptr;  // diagnosis: fp32 direct kernel
+    if (mode == 1 && p->bp_boundary_ok && !precise && !force_direct) {
         float* pyb = scratch;
         const int nvq = (int)p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi;
         float* flatw = scratch + p->n_cols * nvq * kPrefWords;
