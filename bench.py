@@ -332,6 +332,8 @@ def run_sharded(args, cfg, rank, world, local_rank):
     vg, tr = geometry(cfg)
     comm = TorchComm()
     sop = ShardedOperator(vg, tr, comm, device=dev)
+    if args.p2p:  # fused update + all-gather kernels over NVLink peer memory
+        sop.enable_p2p()
     op = sop.op
     truth = op.phantom_internal(P.shepp_logan_3d())
     b_full = op.new_projections()
@@ -408,7 +410,8 @@ def run_sharded(args, cfg, rank, world, local_rank):
         "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
-                   "parallelism": f"A by view x{world}, A^T by cell rows x{world}, NCCL all_gather d/e",
+                   "parallelism": f"A by view x{world}, A^T by cell rows x{world}, " +
+                                  ("fused d/e updates with NVLink peer stores" if args.p2p else "NCCL all_gather d/e"),
                    "l2": "working set > 126 MB L2 (no flush needed)"},
         "ms_A_local": t_a, "ms_AT_local": t_at,
         "roofline": {"bound": "issue", "kernel": dom, "achieved": achieved / 1e9, "peak": peak_slots / 1e9,
@@ -434,6 +437,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--sharded", action="store_true", help="use the sharded (multi-GPU) driver even at N=1")
+    ap.add_argument("--p2p", action="store_true",
+                    help="sharded driver: fused update + NVLink peer stores instead of NCCL all_gathers of d and e")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

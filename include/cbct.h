@@ -168,6 +168,15 @@ int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, const double*
 /* Multi-GPU: *out = vals[0] + vals[1] + ... in index order (the per-rank norm partials after an
  * all_gather), the same fp64 additions as the host's rank-ordered sum. */
 int cbct_sum_ranks(const double* vals, int n, double* out, void* stream);
+/* Multi-GPU fused update + all-gather over NVLink peer memory: the device-scalar updates of
+ * d (resp. e) that also store the rank's new slab into every rank's full-size buffer
+ * (`peers`: a DEVICE array of npeers pointers from a symmetric-memory rendezvous, self
+ * included) at element `offset`; d_own / e_own is the rank's slab of its own buffer.  A device
+ * barrier between ranks must follow before the full vector is read. */
+int cbct_cgls_volume_update_p2p(int64_t n, float* x, const float* d_own, const float* r, const double* scalars,
+                                float* const* peers, int npeers, int64_t offset, void* stream);
+int cbct_cgls_proj_update_p2p(int64_t n, const float* e_own, const float* p, const double* scalars,
+                              double* partials, float* const* peers, int npeers, int64_t offset, void* stream);
 /* Deterministic fixed-order sum of n fp64 partials into *dev_out; if host_out is
  * not NULL the result is also copied there (synchronising the stream). */
 int cbct_reduce_partials(const double* partials, int32_t n, double* dev_out, double* host_out, void* stream);

@@ -178,6 +178,75 @@ __global__ void k_cgls_scalars(double* __restrict__ S, int stage) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused update + all-gather over NVLink peer memory (multi-GPU CGLS).
+// The rank's slab of the new d (or e) is stored into every rank's full-size buffer (peer
+// pointers from the symmetric-memory rendezvous, self included) at the same offset, so the
+// next operator finds the full vector in place after one device barrier: the all_gather's
+// transfer is issued by the update kernel itself, store by store, instead of by a separate
+// collective.  The rank's own slab of its full buffer is its local vector.
+// Same element -> thread map as k_cgls_volume_dev / k_cgls_proj_dev (float4 body + scalar tail),
+// so values and fp64 partial sums are bitwise those of the gathered path.
+__global__ void k_cgls_volume_dev_p2p(int64_t n, float* __restrict__ x, const float* __restrict__ d_own,
+                                      const float* __restrict__ r, const double* __restrict__ S,
+                                      float* const* __restrict__ peers, int npeers, int64_t offset, int use4) {
+    if (S[kSState] != 0.0) return;
+    const float alpha_prev = (float)S[kSAlpha], beta = (float)S[kSBeta];
+    const int do_x = S[kSDoX] != 0.0;
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    const float4* d4 = reinterpret_cast<const float4*>(d_own);
+    const float4* r4 = reinterpret_cast<const float4*>(r);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 dv = d4[i];
+        const float4 rv = r4[i];
+        if (do_x) {
+            float4 xv = x4[i];
+            xv.x = fmaf(alpha_prev, dv.x, xv.x); xv.y = fmaf(alpha_prev, dv.y, xv.y);
+            xv.z = fmaf(alpha_prev, dv.z, xv.z); xv.w = fmaf(alpha_prev, dv.w, xv.w);
+            x4[i] = xv;
+        }
+        dv.x = fmaf(beta, dv.x, rv.x); dv.y = fmaf(beta, dv.y, rv.y);
+        dv.z = fmaf(beta, dv.z, rv.z); dv.w = fmaf(beta, dv.w, rv.w);
+        for (int q = 0; q < npeers; ++q) reinterpret_cast<float4*>(peers[q] + offset)[i] = dv;  // NVLink stores
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float dv = d_own[i];
+        if (do_x) x[i] = fmaf(alpha_prev, dv, x[i]);
+        const float dn = fmaf(beta, dv, r[i]);
+        for (int q = 0; q < npeers; ++q) peers[q][offset + i] = dn;
+    }
+    __threadfence_system();  // the stores are visible to the peers before the barrier that follows
+}
+
+__global__ void k_cgls_proj_dev_p2p(int64_t n, const float* __restrict__ e_own, const float* __restrict__ p,
+                                    const double* __restrict__ S, double* __restrict__ partials,
+                                    float* const* __restrict__ peers, int npeers, int64_t offset, int use4) {
+    if (S[kSState] != 0.0) return;
+    const float a = (float)(-S[kSAlpha]), b = 1.0f;
+    const int64_t n4 = use4 ? n >> 2 : 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    const float4* e4 = reinterpret_cast<const float4*>(e_own);
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 yv = e4[i];
+        const float4 xv = p4[i];
+        yv.x = fmaf(a, xv.x, b * yv.x); yv.y = fmaf(a, xv.y, b * yv.y);
+        yv.z = fmaf(a, xv.z, b * yv.z); yv.w = fmaf(a, xv.w, b * yv.w);
+        for (int q = 0; q < npeers; ++q) reinterpret_cast<float4*>(peers[q] + offset)[i] = yv;
+        sq += (double)yv.x * yv.x + (double)yv.y * yv.y + (double)yv.z * yv.z + (double)yv.w * yv.w;
+    }
+    for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float yv = fmaf(a, p[i], b * e_own[i]);
+        for (int q = 0; q < npeers; ++q) peers[q][offset + i] = yv;
+        sq += (double)yv * yv;
+    }
+    finish(sq, partials);
+    __threadfence_system();
+}
+
 // sum of n per-rank values in index (rank) order: the host loop's `acc += v` sequence, on device
 __global__ void k_sum_ranks(const double* __restrict__ vals, int n, double* __restrict__ out) {
     double acc = 0.0;
@@ -365,6 +434,33 @@ extern "C" int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, co
 extern "C" int cbct_sum_ranks(const double* vals, int n, double* out, void* stream) {
     if (!vals || !out || n < 1) return cbct_fail(CBCT_E_ARG, "cbct_sum_ranks: bad argument");
     k_sum_ranks<<<1, 1, 0, (cudaStream_t)stream>>>(vals, n, out);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_cgls_volume_update_p2p(int64_t n, float* x, const float* d_own, const float* r,
+                                           const double* scalars, float* const* peers, int npeers, int64_t offset,
+                                           void* stream) {
+    if (!x || !d_own || !r || !scalars || !peers || npeers < 1)
+        return cbct_fail(CBCT_E_ARG, "cbct_cgls_volume_update_p2p: bad argument");
+    // float4 body only when every rank's slab is 16-B aligned (peer bases are allocation-aligned)
+    const int use4 = aligned16(x) && aligned16(d_own) && aligned16(r) && (offset & 3) == 0;
+    k_cgls_volume_dev_p2p<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, d_own, r, scalars, peers,
+                                                                                npeers, offset, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_cgls_proj_update_p2p(int64_t n, const float* e_own, const float* p, const double* scalars,
+                                         double* partials, float* const* peers, int npeers, int64_t offset,
+                                         void* stream) {
+    if (!e_own || !p || !scalars || !peers || npeers < 1)
+        return cbct_fail(CBCT_E_ARG, "cbct_cgls_proj_update_p2p: bad argument");
+    const int use4 = aligned16(e_own) && aligned16(p) && (offset & 3) == 0;
+    k_cgls_proj_dev_p2p<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, e_own, p, scalars, partials, peers,
+                                                                              npeers, offset, use4);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();
     return 0;

@@ -129,6 +129,31 @@ class ShardedOperator:
              ctypes.byref(self.op._host), self._s())
         return float(self.op._host.value)
 
+    # ---------------------------------------------- fused updates over peer memory --
+    def enable_p2p(self):
+        """Allocate the full d / e buffers in symmetric memory (peer-addressable over NVLink) so
+        the CGLS vector updates can store their new slab straight into every rank's buffer
+        (cbct_cgls_*_update_p2p) and a device barrier replaces each all_gather."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        group = self.comm.group if self.comm.group is not None else dist.group.WORLD
+        self._d_full = symm_mem.empty(self.n_full, dtype=torch.float32, device=self.device)
+        self._e_full = symm_mem.empty(self.m_full, dtype=torch.float32, device=self.device)
+        self._d_full.zero_()
+        self._e_full.zero_()
+        self._hd = symm_mem.rendezvous(self._d_full, group)
+        self._he = symm_mem.rendezvous(self._e_full, group)
+        self.p2p = True
+        return self
+
+    def d_slab(self):
+        """This rank's slab of the full d buffer (its local d in the fused path)."""
+        return self._d_full[self.rank * self.n_loc:(self.rank + 1) * self.n_loc]
+
+    def e_slab(self):
+        return self._e_full[self.rank * self.m_loc:(self.rank + 1) * self.m_loc]
+
     def gather_volume(self, local):
         return self.comm.all_gather(local, self._d_full)
 
@@ -175,9 +200,12 @@ class DistCglsRun:
         self.t0 = time.perf_counter()
         self.b = b_local
         self.x = torch.zeros(sop.n_loc, dtype=b_local.dtype, device=dev) if x0_local is None else x0_local.clone()
-        self.d = torch.zeros_like(self.x)
+        # fused path: d and e are this rank's slabs of the symmetric full buffers (the NCCL gathers of
+        # the pre-loop below are then in place)
+        self.p2p = getattr(sop, "p2p", False)
+        self.d = sop.d_slab() if self.p2p else torch.zeros_like(self.x)
         self.r = torch.zeros_like(self.x)
-        self.e = torch.zeros_like(b_local)
+        self.e = sop.e_slab() if self.p2p else torch.zeros_like(b_local)
         self.p = torch.zeros_like(b_local)
         self.nb0 = math.sqrt(self.allsum(vec.sumsq(b_local)))
         self.hist = []
@@ -263,17 +291,34 @@ class DistCglsRun:
             _call("cbct_sum_ranks", p(allv), sop.world, p(S[slot:slot + 1]), st())
 
         i0 = self.i
+        if self.p2p:
+            sop.gather_proj(self.e)  # e_full current for the first A^T (the updates keep it so after)
         for _ in range(k):
-            sop.backproject_local(sop.gather_proj(self.e), self.r, norm_out=loc)
+            e_full = sop._e_full if self.p2p else sop.gather_proj(self.e)
+            sop.backproject_local(e_full, self.r, norm_out=loc)
             allsum_into(1)
             _call("cbct_cgls_scalars", p(S), 1, st())
-            _call("cbct_cgls_volume_update_dev", self.d.numel(), p(self.x), p(self.d), p(self.r), p(S), st())
-            sop.project_local(sop.gather_volume(self.d), self.p, norm_out=loc)
+            if self.p2p:  # d update + its all-gather in one kernel, NVLink stores to every rank's buffer
+                _call("cbct_cgls_volume_update_p2p", self.d.numel(), p(self.x), p(self.d), p(self.r), p(S),
+                      ctypes.c_void_p(sop._hd.buffer_ptrs_dev), sop.world, sop.rank * sop.n_loc, st())
+                sop._hd.barrier(channel=0)
+                d_full = sop._d_full
+            else:
+                _call("cbct_cgls_volume_update_dev", self.d.numel(), p(self.x), p(self.d), p(self.r), p(S), st())
+                d_full = sop.gather_volume(self.d)
+            sop.project_local(d_full, self.p, norm_out=loc)
             allsum_into(2)
             _call("cbct_cgls_scalars", p(S), 2, st())
-            _call("cbct_cgls_proj_update_dev", self.e.numel(), p(self.e), p(self.p), p(S),
-                  p(vec.dev.partials), st())
+            if self.p2p:
+                _call("cbct_cgls_proj_update_p2p", self.e.numel(), p(self.e), p(self.p), p(S),
+                      p(vec.dev.partials), ctypes.c_void_p(sop._he.buffer_ptrs_dev), sop.world,
+                      sop.rank * sop.m_loc, st())
+            else:
+                _call("cbct_cgls_proj_update_dev", self.e.numel(), p(self.e), p(self.p), p(S),
+                      p(vec.dev.partials), st())
             _call("cbct_reduce_partials", p(vec.dev.partials), vec.dev.nblocks(self.e.numel()), p(loc), None, st())
+            if self.p2p:
+                sop._he.barrier(channel=0)
             allsum_into(5)
             _call("cbct_cgls_scalars", p(S), 3, st())
         h = S.cpu().numpy()

@@ -124,3 +124,41 @@ def test_nccl_world1_device_resident_loop_is_bitwise_the_host_loop():
             assert torch.equal(devr.x, host.x) and torch.equal(devr.d, host.d) and torch.equal(devr.e, host.e)
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_world1_fused_p2p_updates_are_bitwise_the_gathered_loop():
+    """The fused update + all-gather kernels (stores into every rank's symmetric-memory buffer,
+    device barrier instead of all_gather) give the same iterates as the NCCL-gathered loop.
+    World size 1 here (one GPU): the store loop and the barrier path run, with one peer."""
+    import torch.distributed as dist
+
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200.distributed import CudaVectors, DistCglsRun, ShardedOperator, TorchComm
+    from paper_2110_13526_b200.solvers import SolverConfig
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        d = load_golden("adjoint_instance")
+        vg, tr = geom_from_golden(d)
+        ref_sop = ShardedOperator(vg, tr, TorchComm())
+        b_int = ref_sop.op.new_projections()
+        ref_sop.op.project_internal(ref_sop.op.phantom_internal(P.shepp_logan_3d()), b_int)
+        b_local = torch.zeros(ref_sop.m_loc, device="cuda")
+        b_local[: b_int.numel()] = b_int
+        cfg = SolverConfig(method="cgls", max_iterations=9)
+        base = DistCglsRun(ref_sop, CudaVectors(ref_sop.op), b_local, cfg)
+        base.run_device(9)
+        sop = ShardedOperator(vg, tr, TorchComm()).enable_p2p()
+        fused = DistCglsRun(sop, CudaVectors(sop.op), b_local, cfg)
+        assert fused.p2p
+        fused.run_device(5)
+        fused.run_device(4)
+        assert fused.i == base.i == 9
+        assert [h.rel_discrepancy for h in fused.hist] == [h.rel_discrepancy for h in base.hist]
+        assert torch.equal(fused.x, base.x) and torch.equal(fused.d, base.d) and torch.equal(fused.e, base.e)
+    finally:
+        dist.destroy_process_group()
