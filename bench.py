@@ -286,6 +286,12 @@ def run_ours(args, cfg, rank, world, local_rank):
             "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
             "traffic": traffic.get(kname), "traffic_unit": "B per launch (DRAM read + write, ncu)",
             "traffic_A": traffic.get("k_project_q"),
+            # the HBM view of the same kernel: measured per-launch DRAM bytes over the live kernel time,
+            # against MEASURED_PEAKS.json hbm_gbs (shows the kernel is not HBM-bound)
+            "hbm_gbs": (traffic[kname] / (t_dom * 1e-3) / 1e9) if traffic.get(kname) else None,
+            "hbm_peak_gbs": peaks.get("hbm_gbs"),
+            "hbm_frac": (traffic[kname] / (t_dom * 1e-3) / 1e9 / peaks["hbm_gbs"])
+            if traffic.get(kname) and peaks.get("hbm_gbs") else None,
             "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
                           f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
             "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
