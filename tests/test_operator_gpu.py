@@ -162,6 +162,21 @@ def test_config5_slab_against_oracle():
     _check_random(op, ref)
 
 
+def test_irregular_geometry_against_oracle():
+    """Everything off the beaten path at once: odd, unequal nx/ny/nz, anisotropic voxels, a volume
+    shifted in x, y and z, a fractional principal-point offset and a partial angular span.  The
+    cells are short against the source distance, so the closed-form backprojector and the
+    prefix-sum projector (with its cone-bounded slab windows) are the paths under test."""
+    import paper_2110_13526_b200 as P
+
+    vg = P.VolumeGeometry(97, 83, 61, (0.9, 1.1, 0.7), (7.5, -4.25, 9.3))
+    det = P.DetectorGeometry(211, 157, (1.3, 1.1), (2.37, -3.61))
+    tr = P.make_circular_trajectory(780.0, 1250.0, 5, 0.4, 1.7, det)
+    op, ref = _op(vg, tr), O.OracleOperator(vg, tr)
+    assert op.info.bp_fast_path == 1 and op.info.bp_closed_form == 1
+    _check_random(op, ref)
+
+
 def test_config3_views_against_oracle():
     """BASELINE config 3 (512^3, 720 views, 616x480) on two views: the prefix-sum projector
     at zs = 520 and the closed-form boundary backprojector at 0.43 mm voxels."""
