@@ -25,7 +25,6 @@ import ctypes
 import math
 import time
 
-import numpy as np
 import torch
 
 from ._lib import call
