@@ -9,9 +9,11 @@ a CPU path.  Build it with ``__graft_entry__.build()`` or
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 
-_SO = pathlib.Path(__file__).resolve().parent / "libcbct.so"
+# CBCT_LIBRARY: load another build of the same ABI (A/B timing of kernel variants); default in-tree
+_SO = pathlib.Path(os.environ.get("CBCT_LIBRARY") or pathlib.Path(__file__).resolve().parent / "libcbct.so")
 
 c_i64, c_i32, c_f64, c_f32, c_p = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_float, ctypes.c_void_p
 

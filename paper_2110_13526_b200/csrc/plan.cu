@@ -444,7 +444,7 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         // 3 CTAs per SM (measured: config 2 16+zr 10.3 ms, 16 11.1 ms, 8 14.6 ms; config 3
         // 16 85 ms, 16+zr 103 ms, 12+zr 92 ms)
         auto qsm = [&](int cc, int zr) {
-            return 32 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + (2 * cc + 33) * 4;
+            return 32 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + 3 * (2 * cc + 33) * 4;
         };
         int cq = 16;
         if (const char* e = getenv("CBCT_PROJ_Q_C")) cq = atoi(e);

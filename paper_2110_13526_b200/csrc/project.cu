@@ -321,9 +321,10 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
     constexpr int RZ = ZR ? 1 : 0;
     float* ring = reinterpret_cast<float*>(s_ent + ent_cap);
     constexpr int PC = C <= 8 ? 8 : (C <= 16 ? 16 : 32);  // power-of-two search span
-    float* sB = ring + 2 * (C + RZ) * zs;  // [PC+1] interval starts, chunk end, then +inf padding
-    float* sInv = sB + (PC + 1);          // [C]   1/dtau
-    float* sDl = sInv + C;                // [C]   dtau
+    // three chunk tables of {sB [PC+1]: interval starts, chunk end, then +inf padding; sInv [C]:
+    // 1/dtau; sDl [C]: dtau}
+    constexpr int SBW = PC + 1 + 2 * C;
+    float* sTab = ring + 2 * (C + RZ) * zs;
     const int nwc = (blockDim.x >> 5) - 1;
     const int nct = nwc * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -369,27 +370,40 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                          &full[slot]);
         }
     } else {
-        float chunk_start = h.tau_start;
-        for (int i = 0; i < nch; ++i) {
-            const int slot = i & 1, round = i >> 1;
+        // The chunk tables are triple-buffered: chunk i+1's is written during chunk i's phase 1,
+        // so a single CTA barrier per chunk (after phase 1) orders everything.  A thread writing
+        // table (i+1)%3 has passed barrier i-1, so no thread still reads it (phase 2 of chunk i-2
+        // precedes barrier i-1); the ring slots are ordered by the full/empty mbarriers.
+        auto fill = [&](float* t, int i, float start) {
             const int m0 = i * C, cnt = min(C, M - m0);
             for (int k = threadIdx.x; k <= PC; k += nct) {
-                const float bb = k == 0 ? chunk_start : (k <= cnt ? s_ent[m0 + k - 1].x : INFINITY);
-                sB[k] = bb;
+                const float bb = k == 0 ? start : (k <= cnt ? s_ent[m0 + k - 1].x : INFINITY);
+                t[k] = bb;
                 if (k < cnt) {
                     const float e = s_ent[m0 + k].x;
-                    sInv[k] = e > bb ? 1.0f / (e - bb) : 0.0f;  // fp32-degenerate interval
-                    sDl[k] = e - bb;
+                    t[PC + 1 + k] = e > bb ? 1.0f / (e - bb) : 0.0f;  // fp32-degenerate interval
+                    t[PC + 1 + C + k] = e - bb;
                 }
             }
+        };
+        float chunk_start = h.tau_start;
+        fill(sTab, 0, chunk_start);
+        named_bar(1, nct);
+        int tb = 0;
+        for (int i = 0; i < nch; ++i) {
+            const int slot = i & 1, round = i >> 1;
+            const int cnt = min(C, M - i * C);
+            const float* sB = sTab + tb * SBW;
+            const float* sInv = sB + (PC + 1);
+            const float* sDl = sInv + C;
+            const int tn = tb == 2 ? 0 : tb + 1;
+            const float cend = sB[cnt];
             mbar_wait(&full[slot], round & 1);
-            named_bar(1, nct);  // sB / sDl visible
             // phase 1, in place: row j+1 of the slot becomes Qc[j+1] = sum_{j'<=j} dtau_j' vol_j'
             // (row 0 = Qc[0] = 0), two slabs per thread (float2), only over the slabs some ray of
             // the column can occupy while tau is in this chunk (chunk_slabs; the producer staged
             // exactly that window).
             float* stage = ring + (size_t)slot * slot_elems;
-            const float cend = sB[cnt];
             {
                 const int2 sl = chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
                 const int zs2 = zs >> 1;
@@ -407,7 +421,8 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                     }
                 }
             }
-            named_bar(1, nct);
+            if (i + 1 < nch) fill(sTab + tn * SBW, i + 1, cend);
+            named_bar(1, nct);  // Qc and the next chunk's table visible
             // phase 2: per ray, the slab it ends in plus one correction per z crossing.  The
             // interval search needs no bounds checks (sB is +inf-padded past the chunk end, which
             // the crossing is before).
@@ -440,8 +455,9 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                 s.acc += last[s.iz];
             }
             chunk_start = cend;
-            named_bar(1, nct);  // the slot (now Qc) and sB are reused
-            if (lane == 0) mbar_arrive(&empty[slot]);
+            tb = tn;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
         }
     }
 
@@ -479,7 +495,7 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
         const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
         const int zr = p->proj_q_zr;
         const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * (Cq + zr) * p->zs * 4 +
-                            (size_t)(2 * Cq + 33) * 4;
+                            (size_t)3 * (2 * Cq + 33) * 4;
         const int nt = p->proj_threads + 32;
 #define LAUNCH_Q2(R, CC, Z)                                                                                    \
         do {                                                                                                   \
