@@ -37,6 +37,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // Producer-side wait: back off between polls so a producer blocked on a slot being
 // drained does not take issue slots from the consumer warps of its SM.
+#ifndef CBCT_PRODUCER_SLEEP
+#define CBCT_PRODUCER_SLEEP 64
+#endif
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
     uint32_t done;
     for (;;) {
@@ -50,7 +53,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
         if (done) return;
-        __nanosleep(64);
+        __nanosleep(CBCT_PRODUCER_SLEEP);
     }
 }
 
