@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
                                                       const float* __restrict__ col_scale,
                                                       double* __restrict__ partials, int nv, int nz, int zs,
                                                       double lo2, double p2, double det00z, double pv, int nx,
-                                                      int row0, int row1, int pad_lo, int pad_hi) {
+                                                      int row0, int row1, int pad_lo, int pad_hi,
+                                                      const int32_t* __restrict__ boff, int nb, int vb, int accum) {
     extern __shared__ float s_iw[];  // 2 x nvq rows: 1/rz (pad 0); 1/rz for rz < 0, else -inf
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
     __shared__ int s_vu[kChunk], s_fs[kChunk];
@@ -254,8 +255,13 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
         if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
         return;
     }
-    const int64_t off = cell_off[cell];
-    const int ne = (int)(cell_off[cell + 1] - off);
+    int64_t off = cell_off[cell];
+    int ne = (int)(cell_off[cell + 1] - off);
+    if (boff) {  // view batch vb of nb: a contiguous run of the cell's (column-ordered) entries
+        const int32_t* bo = boff + cell * (nb + 1) + vb;
+        off += bo[0];
+        ne = bo[1] - bo[0];
+    }
     const int nvq = nv + 2 + pad_lo + pad_hi;
     float* s_iwn = s_iw + nvq;
     for (int k = threadIdx.x; TABLE && k < nvq; k += blockDim.x) {
@@ -410,6 +416,7 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
         if (lane < 31 && iz < nz) {
             float val = acc[g];
             if (col_scale) val *= col_scale[lcell * zs + CBCT_ZPAD + iz];
+            if (accum) val += out[CBCT_ZPAD + iz];  // later view batches add to the earlier ones
             out[CBCT_ZPAD + iz] = val;
             sq += (double)val * (double)val;
         }
@@ -454,34 +461,42 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
                 CBCT_CHECK(cudaFuncSetAttribute(k_bp_boundary<G, FL, true>,                                    \
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
                 k_bp_boundary<G, FL, true><<<grid, p->bpg_threads, smem, s>>>(                                 \
-                    p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,  \
+                    p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, part,  \
                     (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,  \
-                    (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi);                                                                               \
+                    (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0);                                                                               \
                 break;                                                                                         \
             }                                                                                                  \
             k_bp_boundary<G, FL, false><<<grid, p->bpg_threads, smem, s>>>(                                    \
-                p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, partials,      \
+                p->d_cell_off, p->d_cell_ent, p->d_cols, p->d_invw, pyb, flatw, vol, col_scale, part,      \
                 (int)p->nv, (int)p->nz, (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx,      \
-                (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi);                                                                                   \
+                (int)row0, (int)row1, p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0);                                                                                   \
         } while (0)
         const bool fl = p->flat_v >= 0;
-        switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
-            case 2: LAUNCH_G(1, false); break;
-            case 3: LAUNCH_G(1, true); break;
-            case 4: LAUNCH_G(2, false); break;
-            case 5: LAUNCH_G(2, true); break;
-            case 6: LAUNCH_G(3, false); break;
-            case 7: LAUNCH_G(3, true); break;
-            case 8: LAUNCH_G(4, false); break;
-            case 9: LAUNCH_G(4, true); break;
-            case 10: LAUNCH_G(5, false); break;
-            case 11: LAUNCH_G(5, true); break;
-            case 12: LAUNCH_G(6, false); break;
-            default: LAUNCH_G(6, true); break;
+        // view batches (plan.bp_vbatch): one launch per batch of views keeps the ray-prefix
+        // columns the resident CTAs gather from closer to L2's size; the last launch writes the
+        // norm partials
+        const int nb = p->bp_vbatch;
+        const int32_t* boff = nb > 1 ? p->d_cell_boff : nullptr;
+        for (int vb = 0; vb < nb; ++vb) {
+            double* part = vb == nb - 1 ? partials : nullptr;
+            switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
+                case 2: LAUNCH_G(1, false); break;
+                case 3: LAUNCH_G(1, true); break;
+                case 4: LAUNCH_G(2, false); break;
+                case 5: LAUNCH_G(2, true); break;
+                case 6: LAUNCH_G(3, false); break;
+                case 7: LAUNCH_G(3, true); break;
+                case 8: LAUNCH_G(4, false); break;
+                case 9: LAUNCH_G(4, true); break;
+                case 10: LAUNCH_G(5, false); break;
+                case 11: LAUNCH_G(5, true); break;
+                case 12: LAUNCH_G(6, false); break;
+                default: LAUNCH_G(6, true); break;
+            }
         }
 #undef LAUNCH_G
         CBCT_CHECK(cudaGetLastError());
-        cbct_count_launch(2);
+        cbct_count_launch(1 + nb);
         return 0;
     }
     const int64_t nr = p->n_rays;

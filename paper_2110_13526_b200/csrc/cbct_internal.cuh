@@ -56,6 +56,8 @@ struct cbct_plan {
     int64_t* d_col_off = nullptr;   // n_cols + 1
     float2* d_col_ent = nullptr;    // {tau_end, __int_as_float(cell_base)} n_intervals
     int64_t* d_cell_off = nullptr;  // n_cells + 1
+    int32_t* d_cell_boff = nullptr;  // n_cells x (bp_vbatch + 1): entry offsets of the view batches in a cell
+    int32_t bp_vbatch = 1;           // A^T launches over view batches (L2 working set)
     CellEntry* d_cell_ent = nullptr;
     double* d_w = nullptr;          // per-row rz (fp64), nv
     float* d_invw = nullptr;        // per-row 1/rz (fp32; +-1e30 for flat rows), nv
