@@ -1,4 +1,4 @@
-"""Kernel-only timing of A and A^T (CUDA events) for a BASELINE config: python tools/time_ops.py [cfg] [reps]."""
+"""Kernel-only timing of A and A^T (CUDA events) for a BASELINE config: python tools/time_ops.py [cfg] [reps] [A|AT]."""
 import os
 import pathlib
 import sys
@@ -33,8 +33,9 @@ def t(fn):
     return s.elapsed_time(e) / reps
 
 
-ta = t(lambda: op.project_internal(x, p))
-tat = t(lambda: op.backproject_internal(y, r, scratch=scr))
+only = sys.argv[3] if len(sys.argv) > 3 else ""  # "A" or "AT": time one operator only
+ta = t(lambda: op.project_internal(x, p)) if only != "AT" else float("nan")
+tat = t(lambda: op.backproject_internal(y, r, scratch=scr)) if only != "A" else float("nan")
 N, V = vg.nx, tr.n_views
 tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("CBCT_"))
 print(f"cfg{cfg} {tag or 'default'}: A {ta:.3f} ms ({N**3*V/ta/1e6:.0f} GUPS)  AT {tat:.3f} ms ({N**3*V/tat/1e6:.0f} GUPS)",
