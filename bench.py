@@ -112,7 +112,8 @@ class ClockSampler:
 
 
 def committed_traffic(cfg: int) -> dict:
-    """Per-launch DRAM bytes of the hot kernels from the committed ncu capture (profiles/traffic_r1.json)."""
+    """DRAM bytes per operator application of the hot kernels from the committed ncu captures
+    (profiles/traffic_r1.json)."""
     try:
         with open(ROOT / "profiles" / "traffic_r1.json") as f:
             return json.load(f).get(f"config{cfg}", {})
@@ -284,9 +285,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     traffic = committed_traffic(cfg)
     roof = {"bound": "issue", "kernel": f"{dom} ({kname})",
             "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
-            "traffic": traffic.get(kname), "traffic_unit": "B per launch (DRAM read + write, ncu)",
+            "traffic": traffic.get(kname),
+            "traffic_unit": "B per operator application (DRAM read + write, ncu; A^T summed over its view-batch launches)",
             "traffic_A": traffic.get("k_project_q"),
-            # the HBM view of the same kernel: measured per-launch DRAM bytes over the live kernel time,
+            # the HBM view of the same kernel: measured DRAM bytes per application over the live time,
             # against MEASURED_PEAKS.json hbm_gbs (shows the kernel is not HBM-bound)
             "hbm_gbs": (traffic[kname] / (t_dom * 1e-3) / 1e9) if traffic.get(kname) else None,
             "hbm_peak_gbs": peaks.get("hbm_gbs"),
