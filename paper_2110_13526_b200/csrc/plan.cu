@@ -392,9 +392,15 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         k_cell_offsets<<<blocks_for(p->n_cells + 1, 256), 256, 0, stream>>>(d_keys_sorted, n, p->n_cells,
                                                                             p->d_cell_off);
         TRYC(cudaGetLastError());
-        // A^T in two view batches once the ray-prefix table outgrows half of L2 (measured: config 2
-        // 14.75 -> 14.46 ms, config 3 131.9 -> 127.6 ms; 4 batches 14.60 / 128.9, 8 batches slower)
-        p->bp_vbatch = (double)p->n_cols * (double)(p->nv + 2) * 8.0 > 64.0 * 1024 * 1024 && p->V >= 2 ? 2 : 1;
+        // A^T in view batches once the ray-prefix table outgrows half of L2: 2 up to 4 GiB, then one
+        // per 2 GiB up to 4 (measured: config 2 14.75 -> 14.46 ms with 2, 3-8 batches slower; config
+        // 3 131.9 -> 127.6 ms with 2, 128.9 with 4; config 5 (9 GB) G=6 1965 ms -> 1679 with 4-6, 1684
+        // with 8, 1703 with 12)
+        {
+            const double tb = (double)p->n_cols * (double)(p->nv + 2) * 8.0;
+            p->bp_vbatch = tb <= 64.0 * 1024 * 1024 ? 1 : (int)std::min(4.0, std::max(2.0, std::floor(tb / 2147483648.0)));
+            p->bp_vbatch = (int)std::min<int64_t>(p->bp_vbatch, p->V);
+        }
         if (const char* e = getenv("CBCT_BP_VBATCH")) p->bp_vbatch = std::max(1, std::min(atoi(e), (int)p->V));
         if (p->bp_vbatch > 1) {
             const int64_t nbo = p->n_cells * (p->bp_vbatch + 1);
@@ -492,16 +498,18 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     p->bp_blocks = (int32_t)(((g->nx + 15) / 16) * ((g->ny + 15) / 16) * 256);  // tiled grid (backproject.cu)
     {
         // 31 voxels per boundary group (32 boundaries = one warp's lanes); a warp runs G
-        // groups so the per-crossing shared loads are amortised (backproject.cu).  Pick
-        // G in [2, 6] covering the groups with the least waste, at most 32 warps.
+        // groups so the per-crossing shared loads are amortised (backproject.cu).  Pick G
+        // covering the groups with the least waste, at most 32 warps, ties to the larger G.
+        // G = 5 is skipped: at the 64-register cap its closed-form instance spills (config 5:
+        // G=5 2169 ms, G=4 1984, G=6 1965 with one view batch).
         const int64_t groups = (g->nz + 30) / 31;
         int best_g = 1;
         int64_t best_waste = INT64_MAX;
-        for (int G = 3; G <= 6; ++G) {
+        for (int G : {3, 4, 6}) {
             const int64_t warps = (groups + G - 1) / G;
             if (warps > 32) continue;
             const int64_t waste = warps * G - groups;
-            if (waste < best_waste) { best_waste = waste; best_g = G; }
+            if (waste <= best_waste) { best_waste = waste; best_g = G; }
         }
         if (best_waste == INT64_MAX) best_g = 6;
         if (groups == 1) best_g = 1;
