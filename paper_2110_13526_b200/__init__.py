@@ -14,7 +14,7 @@ from .phantom import Ellipsoid, Volume, generate_phantom, load_ellipsoids, shepp
 __version__ = "0.1.0"
 
 
-_LAZY = ("operator", "solvers", "analysis", "estimators", "io", "cli")
+_LAZY = ("hostcopy", "operator", "solvers", "analysis", "estimators", "io", "cli")
 
 
 def __getattr__(name):

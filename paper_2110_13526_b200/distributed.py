@@ -27,6 +27,7 @@ import time
 
 import torch
 
+from . import hostcopy
 from ._lib import call
 from .solvers import ConvergenceRecord, SolverReport, SolverConfig
 
@@ -353,6 +354,6 @@ def gathered_report(sop, x_local, info) -> SolverReport:
     from .phantom import Volume
 
     full = sop.gather_volume(x_local)[: sop.op.vol_elems]
-    xr = sop.op.volume_from_internal(full, torch.float64).cpu().numpy()
+    xr = hostcopy.to_host(sop.op.volume_from_internal(full, torch.float64))
     return SolverReport(Volume(sop.op.vol_geom, xr), info["iterations"], info["final_discrepancy_norm"],
                         info["history"], info["worker_count"], info["breakdown"])

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, hostcopy
 from ._lib import CBCT_ZPAD, call, zstride
 from .geometry import TrajectoryGeometry, VolumeGeometry, geometry_key, view_tables
 from .phantom import Volume, coerce_data
@@ -219,7 +219,7 @@ class CbctOperator:
             t = t.contiguous()
         else:
             arr = np.ascontiguousarray(data, dtype=np.float64).ravel()
-            t = torch.from_numpy(arr).to(self.device, non_blocking=False)
+            t = hostcopy.to_device(arr, self.device)  # pinned-staged, threaded (hostcopy.py)
         if t.numel() != size:
             raise ValueError(f"data length {t.numel()} != {size}")
         return t, t.dtype == torch.float64
@@ -302,7 +302,7 @@ class CbctOperator:
                 out.reshape(-1).copy_(res.to(out.dtype))
                 return out
             return res
-        res = convert(t_int, torch.float64).cpu().numpy()
+        res = hostcopy.to_host(convert(t_int, torch.float64))
         if out is not None:
             out[:] = res
             return out
@@ -316,7 +316,7 @@ class CbctOperator:
         self.project_internal(ones, p)
         if internal:
             return InternalProjections(self.trajectory, p)
-        return ProjectionStack(self.trajectory, self.proj_from_internal(p, torch.float64).cpu().numpy())
+        return ProjectionStack(self.trajectory, hostcopy.to_host(self.proj_from_internal(p, torch.float64)))
 
     def col_sums(self, internal: bool = False):
         """A^T 1: per-voxel total traversal length, mm (operator.py:348-351)."""
@@ -325,7 +325,7 @@ class CbctOperator:
         self.backproject_internal(ones, v)
         if internal:
             return InternalVolume(self.vol_geom, v)
-        return Volume(self.vol_geom, self.volume_from_internal(v, torch.float64).cpu().numpy())
+        return Volume(self.vol_geom, hostcopy.to_host(self.volume_from_internal(v, torch.float64)))
 
     def normal_diagonal(self, internal: bool = False):
         """diag(A^T A): per-voxel sum of squared intersection lengths (operator.py:353-362)."""
@@ -333,7 +333,7 @@ class CbctOperator:
         self.backproject_internal(None, v, mode=2)
         if internal:
             return InternalVolume(self.vol_geom, v)
-        return Volume(self.vol_geom, self.volume_from_internal(v, torch.float64).cpu().numpy())
+        return Volume(self.vol_geom, hostcopy.to_host(self.volume_from_internal(v, torch.float64)))
 
     def ray_segments(self, view: int, u: int, v: int):
         """(voxel indices, lengths mm) of the ray through pixel (u, v): A^T of a unit
@@ -345,6 +345,6 @@ class CbctOperator:
         y[(view * det.nu + u) * det.nv + v] = 1.0
         out = self.new_volume()
         self.backproject_internal(y, out)
-        ref = self.volume_from_internal(out, torch.float64).cpu().numpy()
+        ref = hostcopy.to_host(self.volume_from_internal(out, torch.float64))
         idx = np.flatnonzero(ref).astype(np.int64)
         return idx, ref[idx]

@@ -32,6 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import hostcopy
 from ._lib import call
 from .operator import CbctOperator, InternalProjections, InternalVolume
 from .phantom import Volume
@@ -364,7 +365,7 @@ def _final_volume(op, x_int, like):
     """Report the solution in the caller's container kind (numpy fp64 for host b)."""
     if isinstance(like, torch.Tensor) and getattr(like, "is_cuda", False):
         return Volume(op.vol_geom, op.volume_from_internal(x_int, torch.float32))
-    return Volume(op.vol_geom, op.volume_from_internal(x_int, torch.float64).cpu().numpy())
+    return Volume(op.vol_geom, hostcopy.to_host(op.volume_from_internal(x_int, torch.float64)))
 
 
 def _true_rel(op, chain, x_int, b_int, nb0, dev):  # solvers.py:259-261
