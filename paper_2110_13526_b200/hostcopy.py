@@ -11,6 +11,7 @@ and the reported volume, i.e. the host boundary of ``cgls()`` / ``lsqr()`` / ``s
 from __future__ import annotations
 
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
@@ -21,6 +22,7 @@ _THREADS = max(1, min(8, os.cpu_count() or 1))
 _MIN_BYTES = 8 << 20  # below this the plain pageable copy is as fast
 _pool: ThreadPoolExecutor | None = None
 _stages: list[torch.Tensor] = []
+_lock = threading.Lock()  # the stages are shared: one staged copy at a time per process
 
 
 def _workers() -> ThreadPoolExecutor:
@@ -30,7 +32,7 @@ def _workers() -> ThreadPoolExecutor:
     return _pool
 
 
-def _stage(i: int) -> np.ndarray:
+def _stage(i: int) -> torch.Tensor:
     while len(_stages) <= i:
         _stages.append(torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True))
     return _stages[i]
@@ -54,6 +56,11 @@ def to_device(arr: np.ndarray, device) -> torch.Tensor:
     dev = torch.device(device)
     if arr.nbytes < _MIN_BYTES or dev.type != "cuda":
         return torch.from_numpy(arr).to(dev)
+    with _lock:
+        return _to_device_staged(arr, dev)
+
+
+def _to_device_staged(arr: np.ndarray, dev: torch.device) -> torch.Tensor:
     out = torch.empty(arr.size, dtype=torch.from_numpy(arr[:0]).dtype, device=dev)
     per = _CHUNK // arr.itemsize
     side = torch.cuda.Stream(device=dev)
@@ -70,6 +77,9 @@ def to_device(arr: np.ndarray, device) -> torch.Tensor:
             ev = torch.cuda.Event()
             ev.record(side)
         done[k & 1] = ev
+    for ev in done:  # the stages are reused by the next call: their last DMAs must have read them
+        if ev is not None:
+            ev.synchronize()
     torch.cuda.current_stream(dev).wait_stream(side)
     out.record_stream(side)
     return out
@@ -80,6 +90,11 @@ def to_host(t: torch.Tensor) -> np.ndarray:
     t = t.reshape(-1)
     if t.device.type != "cuda" or t.numel() * t.element_size() < _MIN_BYTES:
         return t.cpu().numpy()
+    with _lock:
+        return _to_host_staged(t)
+
+
+def _to_host_staged(t: torch.Tensor) -> np.ndarray:
     res = np.empty(t.numel(), dtype=t.new_empty(0).cpu().numpy().dtype)
     per = _CHUNK // t.element_size()
     dev = t.device

@@ -42,3 +42,12 @@ def test_large_default_path_and_solver_boundary():
     assert torch.equal(d, torch.from_numpy(a).cuda())
     np.testing.assert_array_equal(H.to_host(d), a)
     np.testing.assert_array_equal(H.to_host(d[:10]), a[:10])  # below the staging threshold
+
+
+def test_back_to_back_uploads_do_not_share_in_flight_stages(small_stages):
+    """Consecutive uploads reuse the pinned stages: the previous upload's DMAs must have drained."""
+    H = small_stages
+    arrs = [np.full(4096 * 5 + 3, float(i)) for i in range(6)]
+    outs = [H.to_device(a, "cuda") for a in arrs]
+    for a, d in zip(arrs, outs):
+        np.testing.assert_array_equal(d.cpu().numpy(), a)
