@@ -392,22 +392,22 @@ class CglsRun:
         self.dev = dev = _Dev(op)
         self.chain = chain = _build_chain(op, cfg, dev)
         self.t0 = time.perf_counter()
-        self.b_int = _as_internal_proj(op, b)
         self.x = _alloc(chain.n, chain.n_phys, dev.device)
         self.x.copy_(chain.z_of(_x0_internal(op, cfg, dev)))
         self.d = _alloc(chain.n, chain.n_phys, dev.device)
         self.r = _alloc(chain.n, chain.n_phys, dev.device)
         self.e = _alloc(chain.m, chain.m_phys, dev.device)
         self.p = _alloc(chain.m, chain.m_phys, dev.device)
-        self.b_eff = chain.rhs(self.b_int)
-        self.nb0 = _norm(dev, self.b_int)
         self.history = []
         self.pending = 0.0  # deferred x += alpha*d
         self.i = 0
         self.done = False
         self.breakdown = False
         x, d, r, e, p = self.x, self.d, self.r, self.e, self.p
-        chain.apply(x, p)
+        chain.apply(x, p)  # A x0 needs no b: queued first, it overlaps b's host upload
+        self.b_int = _as_internal_proj(op, b)
+        self.b_eff = chain.rhs(self.b_int)
+        self.nb0 = _norm(dev, self.b_int)
         dev.sub(self.b_eff, p, e)
         self.nr2_old = chain.applyT(e, r, norm2=True)
         if self.nr2_old == 0.0:
