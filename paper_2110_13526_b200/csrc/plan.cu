@@ -461,6 +461,8 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     // two rays per thread: more loads in flight, per-interval overhead shared (measured 10% faster at config 2)
     p->proj_rpt = g->nv <= 64 ? 1 : (g->nv <= 1024 ? 2 : 4);
     if (const char* e = getenv("CBCT_PROJ_RPT")) p->proj_rpt = atoi(e);
+    // the projector kernels run <= 512 ray threads + one producer warp (__launch_bounds__(544))
+    while (p->proj_rpt < 4 && ((g->nv + p->proj_rpt - 1) / p->proj_rpt + 31) / 32 * 32 > 512) p->proj_rpt *= 2;
     p->proj_threads = (int)(((g->nv + p->proj_rpt - 1) / p->proj_rpt + 31) / 32 * 32);
     p->proj_blocks = (int32_t)p->n_cols;
     {
@@ -482,7 +484,10 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         auto qsm = [&](int cc, int zr) {
             return 32 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + 3 * (2 * cc + 33) * 4;
         };
-        int cq = 16;
+        // C = 16 unless two CTAs of it no longer fit an SM's shared memory (zs >~ 800 slabs, i.e.
+        // config 5's 1024 slabs: C=16 1514 ms with one CTA per SM, C=8 1279 ms with two; config
+        // 3, two CTAs either way: C=16 79.4 ms, C=8 94.5)
+        int cq = qsm(16, 0) <= 113 * 1024 ? 16 : 8;
         if (const char* e = getenv("CBCT_PROJ_Q_C")) cq = atoi(e);
         p->proj_q_c = cq;
         p->proj_q_zr = qsm(cq, 1) <= 76 * 1024 ? 1 : 0;
