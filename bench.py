@@ -299,6 +299,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             if traffic.get(kname) and peaks.get("hbm_gbs") else None,
             "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
                           f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
+            # what ncu says binds each kernel (committed capture of the same build): A^T runs the L1/TEX
+            # data path near its peak on the z-row gathers, A is issue / barrier bound
+            "ncu_utilisation": {k: v for k, v in traffic.get("ncu_utilisation", {}).items() if k != "source"} or None,
             "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
             "frac_AT": SLOTS_PER_NNZ * nnz / (t_at * 1e-3) / peak_slots}
     cpu = None
