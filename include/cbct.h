@@ -87,6 +87,11 @@ typedef struct cbct_plan_info {
     int64_t bp_scratch_floats; /* fp32 workspace cbct_backproject needs (scratch_proj) */
     int32_t bp_fast_path;      /* 1: mode-1 A^T uses the boundary-form kernel */
     int32_t bp_closed_form;    /* 1: its straddle fraction is the closed form (no 1/rz table) */
+    /* launch shapes the plan chose (appended; read-only diagnostics) */
+    int32_t proj_chunk;        /* cells per chunk of the prefix-sum projector (0: another projector) */
+    int32_t bp_groups;         /* boundary groups per warp of the boundary-form backprojector */
+    int32_t bp_view_batches;   /* launches of one mode-1 backprojection (view batches) */
+    int32_t reserved;
 } cbct_plan_info;
 
 /* ---- plan lifecycle ------------------------------------------------------ */

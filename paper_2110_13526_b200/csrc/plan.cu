@@ -554,5 +554,9 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->bp_fast_path = p->bp_boundary_ok ? 1 : 0;
     info->bp_closed_form = (p->bp_boundary_ok && p->bp_closed_ok && !getenv("CBCT_BP_TABLE")) ? 1 : 0;
     info->bp_blocks = p->bp_blocks;
+    info->proj_chunk = p->proj_q ? p->proj_q_c : 0;
+    info->bp_groups = p->bpg_groups;
+    info->bp_view_batches = p->bp_vbatch;
+    info->reserved = 0;
     return 0;
 }
