@@ -322,6 +322,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "loop": "device-resident CGLS, CUDA-graph replay per iteration",
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         "setup_s": t_setup, "plan_table_bytes": int(op.info.table_bytes),
+        "plan": {"proj_chunk": int(op.info.proj_chunk), "bp_groups": int(op.info.bp_groups),
+                 "bp_view_batches": int(op.info.bp_view_batches), "bp_closed_form": int(op.info.bp_closed_form)},
         "e_last": run.rel(run.nb),
     }
     if rank == 0:
