@@ -1,4 +1,4 @@
-"""Multi-rank CGLS host logic on CPU: world_size 2 over gloo (no GPU needed).
+"""Multi-rank CGLS host logic on CPU: world_size 2 and 3 over gloo (no GPU needed).
 
 The sharded driver (paper_2110_13526_b200.distributed.dist_cgls) is run with an
 oracle-backed local operator and fp64 torch vectors.  It must reproduce the
@@ -112,13 +112,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_sharded_cgls_world2_matches_single_process():
+@pytest.mark.parametrize("world", [2, 3])  # 3 ranks: uneven view and volume blocks
+def test_sharded_cgls_matches_single_process(world):
     from oracle import oracle as O
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in procs]
