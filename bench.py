@@ -272,9 +272,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         t_solves.append(time.perf_counter() - t0)
     t_e2e = float(np.median(t_solves))
     e2e = {"value": rep.iterations / t_e2e, "unit": "it/s",
-           "h2d_bytes_per_step": int(op.m * 8 / e2e_k), "d2h_bytes_per_step": int((op.n * 8 + 24 * e2e_k) / e2e_k),
+           "h2d_bytes_per_step": int(op.m * 4 / e2e_k), "d2h_bytes_per_step": int((op.n * 8 + 24 * e2e_k) / e2e_k),
            "note": f"cgls() on host fp64 ProjectionStack, K={e2e_k}, incl. pre-loop (2 A + 1 A^T) and the "
-                   f"pinned-staged host copies (hostcopy.py); one untimed warm-up solve; "
+                   f"pinned-staged host copies (hostcopy.py: b narrowed to fp32 on the host, x returned in fp64); "
+                   f"one untimed warm-up solve; "
                    f"median of 3 solves ({', '.join(f'{1e3 * t:.0f}' for t in t_solves)} ms)"}
 
     peaks = measured_peaks()

@@ -38,31 +38,42 @@ def _stage(i: int) -> torch.Tensor:
     return _stages[i]
 
 
+def _copy(dst: np.ndarray, src: np.ndarray) -> None:
+    # a narrowing float cast overflows to +-inf silently, as the device's cvt.rn does
+    # (np.errstate is per thread, so it is set in the worker)
+    with np.errstate(over="ignore"):
+        np.copyto(dst, src, "same_kind")
+
+
 def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
-    """dst[:] = src, split across the worker threads (both 1-D, same dtype and length)."""
+    """dst[:] = src, split across the worker threads (both 1-D, same length)."""
     n = src.size
     if n * src.itemsize < (1 << 20) or _THREADS == 1:
-        np.copyto(dst, src)
+        _copy(dst, src)
         return
     step = -(-n // _THREADS)
-    futs = [_workers().submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    futs = [_workers().submit(_copy, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
     for f in futs:
         f.result()
 
 
-def to_device(arr: np.ndarray, device) -> torch.Tensor:
-    """1-D contiguous numpy array -> device tensor of the same dtype."""
+def to_device(arr: np.ndarray, device, dtype=None) -> torch.Tensor:
+    """1-D numpy array -> device tensor, of ``dtype`` if given (a float narrowing such as fp64 ->
+    fp32 happens in the threaded host copy, round-to-nearest-even like the device's cvt.rn,
+    and halves the bytes that cross PCIe), else of the array's dtype."""
     arr = np.ascontiguousarray(arr).reshape(-1)
+    dt = np.dtype(dtype) if dtype is not None else arr.dtype
     dev = torch.device(device)
     if arr.nbytes < _MIN_BYTES or dev.type != "cuda":
-        return torch.from_numpy(arr).to(dev)
+        with np.errstate(over="ignore"):
+            return torch.from_numpy(arr.astype(dt, copy=False)).to(dev)
     with _lock:
-        return _to_device_staged(arr, dev)
+        return _to_device_staged(arr, dt, dev)
 
 
-def _to_device_staged(arr: np.ndarray, dev: torch.device) -> torch.Tensor:
-    out = torch.empty(arr.size, dtype=torch.from_numpy(arr[:0]).dtype, device=dev)
-    per = _CHUNK // arr.itemsize
+def _to_device_staged(arr: np.ndarray, dt: np.dtype, dev: torch.device) -> torch.Tensor:
+    out = torch.empty(arr.size, dtype=torch.from_numpy(np.empty(0, dt)).dtype, device=dev)
+    per = _CHUNK // max(arr.itemsize, dt.itemsize)
     side = torch.cuda.Stream(device=dev)
     side.wait_stream(torch.cuda.current_stream(dev))  # `out` is allocated on the current stream
     done = [None, None]
@@ -70,7 +81,7 @@ def _to_device_staged(arr: np.ndarray, dev: torch.device) -> torch.Tensor:
         m = min(per, arr.size - off)
         if done[k & 1] is not None:
             done[k & 1].synchronize()  # the DMA that last read this stage has finished
-        stage = _stage(k & 1)[: m * arr.itemsize].view(out.dtype)
+        stage = _stage(k & 1)[: m * dt.itemsize].view(out.dtype)
         _par_copy(stage.numpy(), arr[off:off + m])
         with torch.cuda.stream(side):
             out[off:off + m].copy_(stage, non_blocking=True)

@@ -219,7 +219,9 @@ class CbctOperator:
             t = t.contiguous()
         else:
             arr = np.ascontiguousarray(data, dtype=np.float64).ravel()
-            t = hostcopy.to_device(arr, self.device)  # pinned-staged, threaded (hostcopy.py)
+            # pinned-staged, threaded (hostcopy.py); narrowed to fp32 on the host, bit-identical to
+            # the device conversion and half the PCIe bytes
+            t = hostcopy.to_device(arr, self.device, dtype=np.float32)
         if t.numel() != size:
             raise ValueError(f"data length {t.numel()} != {size}")
         return t, t.dtype == torch.float64

@@ -51,3 +51,21 @@ def test_back_to_back_uploads_do_not_share_in_flight_stages(small_stages):
     outs = [H.to_device(a, "cuda") for a in arrs]
     for a, d in zip(arrs, outs):
         np.testing.assert_array_equal(d.cpu().numpy(), a)
+
+
+def test_host_narrowing_is_bitwise_the_device_conversion(small_stages):
+    """fp64 -> fp32 in the threaded host copy (the operator's upload path) equals the device's
+    cvt.rn.f32.f64 bit for bit, across the fp32 subnormal range, overflow and signed zeros."""
+    H = small_stages
+    rng = np.random.default_rng(11)
+    a = np.concatenate([
+        rng.standard_normal(20000),
+        rng.standard_normal(3000) * 1e-40,              # fp32 subnormal range
+        rng.standard_normal(3000) * 1e-46,              # below it: rounds to +-0 / smallest subnormal
+        rng.standard_normal(1000) * 1e39,               # beyond fp32 max: +-inf
+        np.array([0.0, -0.0, np.inf, -np.inf, 3.4028235677973366e38, 1.0 + 2.0 ** -24]),
+    ])
+    got = H.to_device(a, "cuda", dtype=np.float32)
+    want = torch.from_numpy(a).cuda().float()
+    assert got.dtype == torch.float32
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
