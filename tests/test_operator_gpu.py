@@ -296,3 +296,17 @@ def test_device_tensors_and_reference_signature_abi():
                                                tr.n_views, det.nu, det.nv, *lo, *vg.voxel_size, vg.nx, vg.ny,
                                                vg.nz, 8, 1))
     assert max_rel(acc, d["ATy"]) <= TOL
+
+
+def test_row_and_col_sums_are_the_operator_on_ones():
+    """row_sums is A 1 and col_sums is A^T 1 bit for bit (reference tests/test_operator.py:100-110),
+    on the reference's small_instance geometry (tests/conftest.py:41-51)."""
+    import paper_2110_13526_b200 as P
+
+    vg = P.VolumeGeometry(6, 6, 6, (2.0, 2.0, 2.0))
+    tr = P.make_circular_trajectory(100.0, 200.0, 8, 0.1, 2 * np.pi, P.DetectorGeometry(8, 8, (3.0, 3.0)))
+    op = _op(vg, tr, workers=3)
+    rows = op.row_sums().data
+    np.testing.assert_array_equal(rows, op.project(_vol(op, np.ones(op.n))).data)
+    assert np.all(rows >= 0)
+    np.testing.assert_array_equal(op.col_sums().data, op.backproject(_stack(op, np.ones(op.m))).data)
