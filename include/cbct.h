@@ -193,6 +193,43 @@ int cbct_fill(int64_t n, float* x, float value, void* stream);
 /* Fill a volume's interior with value and its guard slices with 0. */
 int cbct_fill_volume(const cbct_plan* plan, float* vol, float value, void* stream);
 
+/* ---- fp64 reference-precision path (f64.cu) ------------------------------ */
+/* The same operators and vector kernels in fp64 on fp64 device buffers in the same internal
+ * layouts (volume [ny][nx][zs], projections [V][nu][nv]), computed in the reference's
+ * arithmetic (no FMA contraction).  CGLS / LSQR lose orthogonality after ~15-20 iterations
+ * and from then on amplify any rounding difference, so only an fp64 pipeline can follow the
+ * reference's fp64 iterates to 1e-3 over 40 iterations.
+ * cbct_plan_enable_f64 allocates the path's one table (|r| per ray, n_rays fp64) once;
+ * call it before cbct_backproject_f64.
+ * cbct_project_f64: one thread per ray running the reference walk (operator.py:53-187);
+ *   norm2_partials (nullable) receives cbct_f64_proj_blocks(plan) fp64 partials of proj^2.
+ * cbct_backproject_f64: mode 1 A^T proj, mode 2 diag(A^T A) (proj ignored), deterministic
+ *   voxel-driven gather; guards written with 0; col_scale (nullable) multiplies the result;
+ *   norm2_partials receives info.bp_blocks partials. */
+int cbct_plan_enable_f64(cbct_plan* plan, void* stream);
+int cbct_f64_proj_blocks(const cbct_plan* plan);
+int cbct_project_f64(const cbct_plan* plan, const double* vol, double* proj, double* norm2_partials,
+                     void* stream);
+int cbct_backproject_f64(const cbct_plan* plan, const double* proj, double* vol, int mode, const double* col_scale,
+                         double* norm2_partials, void* stream);
+int cbct_volume_to_internal_f64(const cbct_plan* plan, const double* src, double* dst, void* stream);
+int cbct_volume_from_internal_f64(const cbct_plan* plan, const double* src, double* dst, void* stream);
+int cbct_proj_to_internal_f64(const cbct_plan* plan, const double* src, double* dst, void* stream);
+int cbct_proj_from_internal_f64(const cbct_plan* plan, const double* src, double* dst, void* stream);
+/* fp64 vector kernels, as their fp32 counterparts above (partials: cbct_f64_vec_blocks(n)). */
+int cbct_f64_vec_blocks(int64_t n);
+int cbct_axpby_f64(int64_t n, double a, const double* x, double b, double* y, double* partials, void* stream);
+int cbct_scale_div_f64(int64_t n, double* y, double d, double* partials, void* stream); /* y /= d */
+int cbct_sub_f64(int64_t n, const double* a, const double* b, double* out, double* partials, void* stream);
+int cbct_dot_f64(int64_t n, const double* x, const double* y, double* partials, void* stream);
+int cbct_mul_f64(int64_t n, const double* a, const double* b, double* out, void* stream);
+/* if do_x: x = x + alpha_prev*d ;  d = d*beta + r  (CGLS, solvers.py:340-341, 354-355; also LSQR's
+ * x += (phi/rho) w ; w *= -(theta/rho) ; w += v, solvers.py:451-453) */
+int cbct_cgls_volume_update_f64(int64_t n, double* x, double* d, const double* r, double alpha_prev, int do_x,
+                                double beta, void* stream);
+int cbct_fill_volume_f64(const cbct_plan* plan, double* vol, double value, void* stream);
+int cbct_clip_f64(const cbct_plan* plan, double* vol, double lo, double hi, void* stream);
+
 /* ---- phantom voxelizer ------------------------------- */
 /* Replaces generate_phantom (phantom.py:87-106): sum of the intensities of the
  * ellipsoids containing each voxel centre (phantom.py:78-84), bit-identical to the

@@ -87,6 +87,23 @@ SIGNATURES = {
     "cbct_ref_backproject": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_p, c_i64, c_i64, c_i64,
                                      c_f64, c_f64, c_f64, c_f64, c_f64, c_f64, c_i64, c_i64, c_i64,
                                      c_i64, c_i32]),
+    "cbct_plan_enable_f64": (c_i32, [c_p, c_p]),
+    "cbct_f64_proj_blocks": (c_i32, [c_p]),
+    "cbct_project_f64": (c_i32, [c_p, c_p, c_p, c_p, c_p]),
+    "cbct_backproject_f64": (c_i32, [c_p, c_p, c_p, c_i32, c_p, c_p, c_p]),
+    "cbct_volume_to_internal_f64": (c_i32, [c_p, c_p, c_p, c_p]),
+    "cbct_volume_from_internal_f64": (c_i32, [c_p, c_p, c_p, c_p]),
+    "cbct_proj_to_internal_f64": (c_i32, [c_p, c_p, c_p, c_p]),
+    "cbct_proj_from_internal_f64": (c_i32, [c_p, c_p, c_p, c_p]),
+    "cbct_f64_vec_blocks": (c_i32, [c_i64]),
+    "cbct_axpby_f64": (c_i32, [c_i64, c_f64, c_p, c_f64, c_p, c_p, c_p]),
+    "cbct_scale_div_f64": (c_i32, [c_i64, c_p, c_f64, c_p, c_p]),
+    "cbct_sub_f64": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_dot_f64": (c_i32, [c_i64, c_p, c_p, c_p, c_p]),
+    "cbct_mul_f64": (c_i32, [c_i64, c_p, c_p, c_p, c_p]),
+    "cbct_cgls_volume_update_f64": (c_i32, [c_i64, c_p, c_p, c_p, c_f64, c_i32, c_f64, c_p]),
+    "cbct_fill_volume_f64": (c_i32, [c_p, c_p, c_f64, c_p]),
+    "cbct_clip_f64": (c_i32, [c_p, c_p, c_f64, c_f64, c_p]),
     "cbct_last_error": (ctypes.c_char_p, []),
     "cbct_version": (c_i32, []),
     "cbct_launch_count": (c_i64, []),

@@ -59,6 +59,14 @@ struct cbct_plan {
     int32_t* d_cell_boff = nullptr;  // n_cells x (bp_vbatch + 1): entry offsets of the view batches in a cell
     int32_t bp_vbatch = 1;           // A^T launches over view batches (L2 working set)
     CellEntry* d_cell_ent = nullptr;
+    double* d_srcs = nullptr;       // per-view tables of _view_tables (operator.py:262-281), [V][3] fp64
+    double* d_det00 = nullptr;
+    double* d_ustep = nullptr;
+    double* d_vstep = nullptr;
+    double* d_len64 = nullptr;      // fp64 path (f64.cu): |r| per ray, internal order; cbct_plan_enable_f64
+    void* d_rayz64 = nullptr;       // fp64 path: per-ray box clip and z-walk start (f64.cu RayZ)
+    void* d_rayiz64 = nullptr;      // fp64 path: per-ray entry slab and z step (int2)
+    void* d_cell_t64 = nullptr;     // fp64 path: per cell entry, the column walk's t bounding the crossing
     double* d_w = nullptr;          // per-row rz (fp64), nv
     float* d_invw = nullptr;        // per-row 1/rz (fp32; +-1e30 for flat rows), nv
     // launch shapes

@@ -276,6 +276,14 @@ extern "C" int cbct_plan_destroy(cbct_plan* p) {
     cudaFree(p->d_cell_ent);
     cudaFree(p->d_w);
     cudaFree(p->d_invw);
+    cudaFree(p->d_srcs);
+    cudaFree(p->d_det00);
+    cudaFree(p->d_ustep);
+    cudaFree(p->d_vstep);
+    cudaFree(p->d_len64);
+    cudaFree(p->d_rayz64);
+    cudaFree(p->d_rayiz64);
+    cudaFree(p->d_cell_t64);
     delete p;
     return 0;
 }
@@ -291,6 +299,19 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     const int64_t zs = (g->nz + 2 * CBCT_ZPAD + 3) / 4 * 4;  // 16-B aligned cell columns (TMA)
     if (g->nx * g->ny * zs >= (int64_t)INT32_MAX)
         return cbct_fail(CBCT_E_GEOMETRY, "volume too large for 32-bit cell offsets on one device");
+    // Launch-shape limits, checked here so an unsupported size fails at construction with a
+    // clear message instead of a generic launch error at the first A / A^T call:
+    //  * projector: <= 4 rays per thread and <= 512 ray threads + 1 producer warp
+    //    (__launch_bounds__(544), project.cu)  ->  nv <= 2048;
+    //  * direct backprojector (mode 2 / normal_diagonal): <= 4 voxels per thread and
+    //    <= 512 threads (__launch_bounds__(512), backproject.cu)  ->  nz <= 2048;
+    //  * layout transposes put the view index in gridDim.z (layout.cu)  ->  n_views <= 65535.
+    if (g->nv > 2048)
+        return cbct_fail(CBCT_E_GEOMETRY, "cbct_plan_create: detector rows nv > 2048 are not supported");
+    if (g->nz > 2048)
+        return cbct_fail(CBCT_E_GEOMETRY, "cbct_plan_create: volume slices nz > 2048 are not supported");
+    if (g->n_views > 65535)
+        return cbct_fail(CBCT_E_GEOMETRY, "cbct_plan_create: more than 65535 views are not supported");
     const int64_t V = g->n_views;
     // The circular-trajectory family (geometry.py:144-164): source z = 0, u axis
     // horizontal, v axis = +z with one common pitch and one common det00 z.
@@ -332,12 +353,18 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
 #define TRYC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { rc = cbct_fail_cuda(_e, #x); goto fail; } } while (0)
     {
         const size_t tb = (size_t)V * 3 * sizeof(double);
-        TRY(dev_alloc(&d_srcs, V * 3, nullptr));
-        TRY(dev_alloc(&d_det00, V * 3, nullptr));
-        TRY(dev_alloc(&d_ustep, V * 3, nullptr));
+        // the plan keeps the per-view tables (the fp64 path, f64.cu, walks rays from them)
+        TRY(dev_alloc(&p->d_srcs, V * 3, nullptr));
+        TRY(dev_alloc(&p->d_det00, V * 3, nullptr));
+        TRY(dev_alloc(&p->d_ustep, V * 3, nullptr));
+        d_srcs = p->d_srcs;
+        d_det00 = p->d_det00;
+        d_ustep = p->d_ustep;
         TRYC(cudaMemcpyAsync(d_srcs, g->srcs, tb, cudaMemcpyHostToDevice, stream));
         TRYC(cudaMemcpyAsync(d_det00, g->det00, tb, cudaMemcpyHostToDevice, stream));
         TRYC(cudaMemcpyAsync(d_ustep, g->ustep, tb, cudaMemcpyHostToDevice, stream));
+        TRY(dev_alloc(&p->d_vstep, V * 3, nullptr));
+        TRYC(cudaMemcpyAsync(p->d_vstep, g->vstep, tb, cudaMemcpyHostToDevice, stream));
 
         GeomDev gd{g->lo[0], g->lo[1], g->pitch[0], g->pitch[1], g->nx, g->ny, g->nu, zs};
         TRY(dev_alloc(&p->d_cols, p->n_cols, &total));
@@ -523,12 +550,12 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         p->bpg_threads = (int)(((groups + best_g - 1) / best_g) * 32);
     }
     p->table_bytes = total;
-    cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);
+    cudaFree(d_counts); cudaFree(d_cellkey);  // d_srcs/d_det00/d_ustep belong to the plan
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
     *out = p;
     return 0;
 fail:
-    cudaFree(d_srcs); cudaFree(d_det00); cudaFree(d_ustep); cudaFree(d_counts); cudaFree(d_cellkey);
+    cudaFree(d_counts); cudaFree(d_cellkey);  // d_srcs/d_det00/d_ustep belong to the plan
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
     cudaFree(d_tmp);
     cbct_plan_destroy(p);

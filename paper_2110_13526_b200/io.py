@@ -211,6 +211,7 @@ def _stream_to_device(fh, nbytes: int, device):
     stages = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     done = [None, None]
     side = torch.cuda.Stream(device=dev)
+    side.wait_stream(torch.cuda.current_stream(dev))  # `out` is allocated on the current stream
     off, k = 0, 0
     while off < nbytes:
         n = min(chunk, nbytes - off)
@@ -228,6 +229,7 @@ def _stream_to_device(fh, nbytes: int, device):
         off += n
         k += 1
     torch.cuda.current_stream(dev).wait_stream(side)
+    out.record_stream(side)
     return out
 
 

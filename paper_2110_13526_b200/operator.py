@@ -20,6 +20,7 @@ Containers passed in decide what comes back:
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -30,7 +31,10 @@ from ._lib import CBCT_ZPAD, call, zstride
 from .geometry import TrajectoryGeometry, VolumeGeometry, geometry_key, view_tables
 from .phantom import Volume, coerce_data
 
-__all__ = ["GeometryMismatchError", "ProjectionStack", "CbctOperator", "InternalVolume", "InternalProjections"]
+__all__ = ["GeometryMismatchError", "ProjectionStack", "CbctOperator", "InternalVolume", "InternalProjections",
+           "PRECISIONS"]
+
+PRECISIONS = ("f32", "f64")
 
 
 class GeometryMismatchError(ValueError):
@@ -95,14 +99,21 @@ class CbctOperator:
     deterministic gather, so results are bitwise reproducible for any value.
     """
 
-    def __init__(self, vol_geom, trajectory, workers: int = 8, device=None):
+    def __init__(self, vol_geom, trajectory, workers: int = 8, device=None, precision: str = "f32"):
         if workers < 1:
             raise ValueError("workers must be >= 1")
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}, got {precision!r}")
         if not torch.cuda.is_available():
             raise RuntimeError("CbctOperator needs a CUDA device (libcbct.so has no CPU path)")
         self.vol_geom = vol_geom
         self.trajectory = trajectory
         self.workers = int(workers)
+        # "f32": the fast path (fp32 buffers, csrc/project.cu + backproject.cu + vec.cu).
+        # "f64": the reference-precision path (fp64 buffers and arithmetic, csrc/f64.cu), which
+        # follows the reference's fp64 Krylov iterates to its own reproducibility floor.
+        self.precision = precision
+        self.dtype = torch.float64 if precision == "f64" else torch.float32
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._vkey = geometry_key(vol_geom)
         self._tkey = geometry_key(trajectory)
@@ -121,16 +132,43 @@ class CbctOperator:
         with torch.cuda.device(self.device):
             call("cbct_plan_create", ctypes.byref(plan), ctypes.byref(g), self._stream())
         self._plan = plan
+        if self.f64:
+            with torch.cuda.device(self.device):
+                call("cbct_plan_enable_f64", plan, self._stream())
         info = _lib.PlanInfo()
         call("cbct_plan_get_info", plan, ctypes.byref(info))
         self.info = info
         self.vol_elems = int(info.vol_elems)
         self.zstride = int(info.zstride)
-        nred = max(int(info.proj_blocks), int(info.bp_blocks),
-                   _lib.lib().cbct_vec_blocks(max(self.vol_elems, int(info.n_rays))))
-        self._partials = torch.empty(nred, dtype=torch.float64, device=self.device)
-        self._red = torch.empty(1, dtype=torch.float64, device=self.device)
-        self._host = ctypes.c_double(0.0)
+        self._nred = max(int(info.proj_blocks), int(info.bp_blocks),
+                         _lib.lib().cbct_vec_blocks(max(self.vol_elems, int(info.n_rays))),
+                         _lib.lib().cbct_f64_vec_blocks(max(self.vol_elems, int(info.n_rays))),
+                         _lib.lib().cbct_f64_proj_blocks(plan))
+        self._tls = threading.local()
+
+    # Norm-reduction scratch (per-CTA fp64 partials, the reduced device scalar and its host
+    # copy) is per thread: the reference documents its operator as safe to share across
+    # threads (operator.py:284-290), and two solves on one operator must not read each
+    # other's partials.
+    def _scratch(self):
+        s = getattr(self._tls, "s", None)
+        if s is None:
+            s = (torch.empty(self._nred, dtype=torch.float64, device=self.device),
+                 torch.empty(1, dtype=torch.float64, device=self.device), ctypes.c_double(0.0))
+            self._tls.s = s
+        return s
+
+    @property
+    def _partials(self) -> torch.Tensor:
+        return self._scratch()[0]
+
+    @property
+    def _red(self) -> torch.Tensor:
+        return self._scratch()[1]
+
+    @property
+    def _host(self) -> ctypes.c_double:
+        return self._scratch()[2]
 
     def __del__(self):
         plan = getattr(self, "_plan", None)
@@ -143,12 +181,16 @@ class CbctOperator:
 
     def __deepcopy__(self, memo):
         # sklearn.clone deep-copies estimators (test_estimators.py:35-43): rebuild the plan.
-        return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device)
+        return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device, self.precision)
 
     def __reduce__(self):
         # pickling (joblib workers of sklearn model selection) carries the geometry; the device
         # plan is rebuilt on load
-        return (CbctOperator, (self.vol_geom, self.trajectory, self.workers, str(self.device)))
+        return (CbctOperator, (self.vol_geom, self.trajectory, self.workers, str(self.device), self.precision))
+
+    @property
+    def f64(self) -> bool:
+        return self.precision == "f64"
 
     # ------------------------------------------------------------ properties --
     @property
@@ -165,20 +207,31 @@ class CbctOperator:
 
     # ------------------------------------------------- device-layout helpers --
     def new_volume(self) -> torch.Tensor:
-        return torch.zeros(self.vol_elems, dtype=torch.float32, device=self.device)
+        return torch.zeros(self.vol_elems, dtype=self.dtype, device=self.device)
 
     def new_bp_scratch(self) -> torch.Tensor:
-        """Workspace of cbct_backproject (per-column prefix sums)."""
-        return torch.empty(int(self.info.bp_scratch_floats), dtype=torch.float32, device=self.device)
+        """Workspace of cbct_backproject (per-column prefix sums; the fp64 path needs none)."""
+        n = 1 if self.f64 else int(self.info.bp_scratch_floats)
+        return torch.empty(n, dtype=torch.float32, device=self.device)
+
+    def fill_volume(self, vol: torch.Tensor, value: float) -> None:
+        """Interior = value, guard slices = 0."""
+        if self.f64:
+            call("cbct_fill_volume_f64", self._plan, _ptr(vol), ctypes.c_double(value), self._stream())
+        else:
+            call("cbct_fill_volume", self._plan, _ptr(vol), ctypes.c_float(value), self._stream())
 
     def new_projections(self) -> torch.Tensor:
-        return torch.zeros(self.m, dtype=torch.float32, device=self.device)
+        return torch.zeros(self.m, dtype=self.dtype, device=self.device)
 
     def volume_to_internal(self, data, out=None) -> torch.Tensor:
         """Reference-layout volume (numpy fp64 or torch) -> device layout."""
         out = self.new_volume() if out is None else out
         src, f64 = self._device_src(data, self.n)
-        call("cbct_volume_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
+        if self.f64:
+            call("cbct_volume_to_internal_f64", self._plan, _ptr(src), _ptr(out), self._stream())
+        else:
+            call("cbct_volume_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
         return out
 
     def phantom_internal(self, ellipsoids, out=None) -> torch.Tensor:
@@ -189,11 +242,21 @@ class CbctOperator:
         ellipsoids = list(ellipsoids)
         out = self.new_volume() if out is None else out
         params = _device_params(ellipsoids, self.device)
+        if self.f64:  # fp64 sums in the reference layout, then the device layout
+            g = self.vol_geom
+            ref = torch.empty(self.n, dtype=torch.float64, device=self.device)
+            call("cbct_phantom_ref_f64", g.nx, g.ny, g.nz, _ptr(params) if ellipsoids else None, len(ellipsoids),
+                 _ptr(ref), self._stream())
+            return self.volume_to_internal(ref, out)
         call("cbct_phantom", self._plan, _ptr(params) if ellipsoids else None, len(ellipsoids), _ptr(out),
              self._stream())
         return out
 
     def volume_from_internal(self, t: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
+        if self.f64:
+            out = torch.empty(self.n, dtype=torch.float64, device=self.device)
+            call("cbct_volume_from_internal_f64", self._plan, _ptr(t), _ptr(out), self._stream())
+            return out if dtype == torch.float64 else out.to(dtype)
         out = torch.empty(self.n, dtype=dtype, device=self.device)
         call("cbct_volume_from_internal", self._plan, _ptr(t), _ptr(out), int(dtype == torch.float64),
              self._stream())
@@ -202,10 +265,17 @@ class CbctOperator:
     def proj_to_internal(self, data, out=None) -> torch.Tensor:
         out = self.new_projections() if out is None else out
         src, f64 = self._device_src(data, self.m)
-        call("cbct_proj_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
+        if self.f64:
+            call("cbct_proj_to_internal_f64", self._plan, _ptr(src), _ptr(out), self._stream())
+        else:
+            call("cbct_proj_to_internal", self._plan, _ptr(src), int(f64), _ptr(out), self._stream())
         return out
 
     def proj_from_internal(self, t: torch.Tensor, dtype=torch.float32) -> torch.Tensor:
+        if self.f64:
+            out = torch.empty(self.m, dtype=torch.float64, device=self.device)
+            call("cbct_proj_from_internal_f64", self._plan, _ptr(t), _ptr(out), self._stream())
+            return out if dtype == torch.float64 else out.to(dtype)
         out = torch.empty(self.m, dtype=dtype, device=self.device)
         call("cbct_proj_from_internal", self._plan, _ptr(t), _ptr(out), int(dtype == torch.float64),
              self._stream())
@@ -214,14 +284,16 @@ class CbctOperator:
     def _device_src(self, data, size):
         if isinstance(data, torch.Tensor):
             t = data.reshape(-1)
-            if t.device != self.device or t.dtype not in (torch.float32, torch.float64):
+            if self.f64:
+                t = t.to(self.device, torch.float64)
+            elif t.device != self.device or t.dtype not in (torch.float32, torch.float64):
                 t = t.to(self.device, torch.float32)
             t = t.contiguous()
         else:
             arr = np.ascontiguousarray(data, dtype=np.float64).ravel()
-            # pinned-staged, threaded (hostcopy.py); narrowed to fp32 on the host, bit-identical to
-            # the device conversion and half the PCIe bytes
-            t = hostcopy.to_device(arr, self.device, dtype=np.float32)
+            # pinned-staged, threaded (hostcopy.py); the fp32 path narrows to fp32 on the host,
+            # bit-identical to the device conversion and half the PCIe bytes
+            t = hostcopy.to_device(arr, self.device, dtype=np.float64 if self.f64 else np.float32)
         if t.numel() != size:
             raise ValueError(f"data length {t.numel()} != {size}")
         return t, t.dtype == torch.float64
@@ -232,19 +304,28 @@ class CbctOperator:
         With ``norm_out`` (a 1-element fp64 device tensor) the norm is reduced into it on the
         device instead, with no host round trip (device-resident solver loops)."""
         part = self._partials if (norm2 or norm_out is not None) else None
-        call("cbct_project", self._plan, _ptr(x), _ptr(out), _ptr(part), self._stream())
+        if self.f64:
+            call("cbct_project_f64", self._plan, _ptr(x), _ptr(out), _ptr(part), self._stream())
+            nparts = _lib.lib().cbct_f64_proj_blocks(self._plan)
+        else:
+            call("cbct_project", self._plan, _ptr(x), _ptr(out), _ptr(part), self._stream())
+            nparts = int(self.info.proj_blocks)
         if norm_out is not None:
-            return self.reduce_to(int(self.info.proj_blocks), norm_out)
-        return self.reduce(int(self.info.proj_blocks)) if norm2 else None
+            return self.reduce_to(nparts, norm_out)
+        return self.reduce(nparts) if norm2 else None
 
     def backproject_internal(self, y, out: torch.Tensor, mode: int = 1, norm2: bool = False, col_scale=None,
                              scratch=None, norm_out=None):
         """out = A^T y (mode 1) or diag(A^T A) (mode 2, y ignored); ||out||^2 if norm2 (or, with
         ``norm_out``, reduced on the device into that 1-element fp64 tensor)."""
-        scratch = self.new_bp_scratch() if scratch is None else scratch
         part = self._partials if (norm2 or norm_out is not None) else None
-        call("cbct_backproject", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode), _ptr(scratch),
-             _ptr(col_scale), _ptr(part), self._stream())
+        if self.f64:
+            call("cbct_backproject_f64", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode),
+                 _ptr(col_scale), _ptr(part), self._stream())
+        else:
+            scratch = self.new_bp_scratch() if scratch is None else scratch
+            call("cbct_backproject", self._plan, _ptr(y) if mode == 1 else None, _ptr(out), int(mode),
+                 _ptr(scratch), _ptr(col_scale), _ptr(part), self._stream())
         if norm_out is not None:
             return self.reduce_to(int(self.info.bp_blocks), norm_out)
         return self.reduce(int(self.info.bp_blocks)) if norm2 else None
@@ -255,9 +336,10 @@ class CbctOperator:
 
     def reduce(self, n_partials: int) -> float:
         """Deterministic sum of the first n partials (synchronises the stream)."""
-        call("cbct_reduce_partials", _ptr(self._partials), int(n_partials), _ptr(self._red),
-             ctypes.byref(self._host), self._stream())
-        return float(self._host.value)
+        partials, red, host = self._scratch()
+        call("cbct_reduce_partials", _ptr(partials), int(n_partials), _ptr(red), ctypes.byref(host),
+             self._stream())
+        return float(host.value)
 
     # ------------------------------------------------------------ public API --
     def _check_vol(self, x):
@@ -299,7 +381,7 @@ class CbctOperator:
     def _emit(self, convert, t_int, like, out, size):
         """Convert a device-layout result back to the caller's kind of container."""
         if isinstance(like, torch.Tensor):
-            res = convert(t_int, torch.float32)
+            res = convert(t_int, self.dtype)
             if out is not None:
                 out.reshape(-1).copy_(res.to(out.dtype))
                 return out
@@ -313,7 +395,7 @@ class CbctOperator:
     def row_sums(self, internal: bool = False):
         """A 1: per-ray chord length through the volume box, mm (operator.py:343-346)."""
         ones = self.new_volume()
-        call("cbct_fill_volume", self._plan, _ptr(ones), ctypes.c_float(1.0), self._stream())
+        self.fill_volume(ones, 1.0)
         p = self.new_projections()
         self.project_internal(ones, p)
         if internal:
@@ -322,7 +404,7 @@ class CbctOperator:
 
     def col_sums(self, internal: bool = False):
         """A^T 1: per-voxel total traversal length, mm (operator.py:348-351)."""
-        ones = torch.ones(self.m, dtype=torch.float32, device=self.device)
+        ones = torch.ones(self.m, dtype=self.dtype, device=self.device)
         v = self.new_volume()
         self.backproject_internal(ones, v)
         if internal:

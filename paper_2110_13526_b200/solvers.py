@@ -113,10 +113,11 @@ class SolverReport:
     breakdown: bool = False
 
 
-def _alloc(size: int, physical: int = None, device=None) -> torch.Tensor:
+def _alloc(size: int, physical: int = None, device=None, dtype=torch.float32) -> torch.Tensor:
     """Allocation funnel for the solver work vectors (auditable, solvers.py:118-120).
-    ``size`` is the logical length (n or m); ``physical`` the padded device length."""
-    return torch.zeros(physical if physical is not None else size, dtype=torch.float32, device=device)
+    ``size`` is the logical length (n or m); ``physical`` the padded device length; ``dtype``
+    the operator's precision (fp32 fast path, fp64 reference-precision path)."""
+    return torch.zeros(physical if physical is not None else size, dtype=dtype, device=device)
 
 
 def _p(t):
@@ -124,7 +125,9 @@ def _p(t):
 
 
 class _Dev:
-    """Fused vector kernels of libcbct bound to an operator's stream and partials."""
+    """Fused vector kernels of libcbct bound to an operator's stream and partials.  An fp64
+    operator (``precision="f64"``) gets the fp64 kernels of csrc/f64.cu, which round like the
+    reference's NumPy updates."""
 
     def __init__(self, op):
         self.op = op
@@ -133,9 +136,15 @@ class _Dev:
         self.partials = op._partials
         self.vol_elems = op.vol_elems
         self.device = op.device
+        self.dtype = getattr(op, "dtype", torch.float32)
+        self.f64 = self.dtype == torch.float64
+        self._sfx = "_f64" if self.f64 else ""
 
     def s(self):
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def empty(self, n):
+        return torch.empty(n, dtype=self.dtype, device=self.device)
 
     def reduce(self, nparts: int) -> float:
         return self.op.reduce(nparts)
@@ -143,37 +152,51 @@ class _Dev:
     def nblocks(self, n):
         from ._lib import lib
 
-        return lib().cbct_vec_blocks(n)
+        return lib().cbct_f64_vec_blocks(n) if self.f64 else lib().cbct_vec_blocks(n)
 
     def axpby(self, a, x, b, y, norm2=False):
-        call("cbct_axpby", y.numel(), float(a), _p(x), float(b), _p(y), _p(self.partials) if norm2 else None,
-             self.s())
+        call("cbct_axpby" + self._sfx, y.numel(), float(a), _p(x), float(b), _p(y),
+             _p(self.partials) if norm2 else None, self.s())
+        return self.reduce(self.nblocks(y.numel())) if norm2 else None
+
+    def div(self, y, d, norm2=False):
+        """y /= d (u /= beta and friends, solvers.py:407-441); the fp32 path multiplies by 1/d."""
+        if not self.f64:
+            return self.axpby(0.0, None, 1.0 / d, y, norm2=norm2)
+        call("cbct_scale_div_f64", y.numel(), _p(y), float(d), _p(self.partials) if norm2 else None, self.s())
         return self.reduce(self.nblocks(y.numel())) if norm2 else None
 
     def sumsq(self, y):
         return self.axpby(0.0, None, 1.0, y, norm2=True)
 
     def sub(self, a, b, out, norm2=False):
-        call("cbct_sub", out.numel(), _p(a), _p(b), _p(out), _p(self.partials) if norm2 else None, self.s())
+        call("cbct_sub" + self._sfx, out.numel(), _p(a), _p(b), _p(out), _p(self.partials) if norm2 else None,
+             self.s())
         return self.reduce(self.nblocks(out.numel())) if norm2 else None
 
     def dot(self, x, y):
-        call("cbct_dot", x.numel(), _p(x), _p(y), _p(self.partials), self.s())
+        call("cbct_dot" + self._sfx, x.numel(), _p(x), _p(y), _p(self.partials), self.s())
         return self.reduce(self.nblocks(x.numel()))
 
     def mul(self, a, b, out):
-        call("cbct_mul", out.numel(), _p(a), _p(b), _p(out), self.s())
+        call("cbct_mul" + self._sfx, out.numel(), _p(a), _p(b), _p(out), self.s())
 
     def update2(self, x, d, r, a_prev, do_x, beta):
         """x += a_prev*d (if do_x); d = r + beta*d  -- one fused pass."""
-        call("cbct_cgls_volume_update", d.numel(), _p(x), _p(d), _p(r), float(a_prev), int(do_x), float(beta),
-             self.s())
+        call("cbct_cgls_volume_update" + self._sfx, d.numel(), _p(x), _p(d), _p(r), float(a_prev), int(do_x),
+             float(beta), self.s())
 
     def clip(self, vol, lo, hi):
-        call("cbct_clip", self.plan, _p(vol), ctypes.c_float(lo), ctypes.c_float(hi), self.s())
+        if self.f64:
+            call("cbct_clip_f64", self.plan, _p(vol), ctypes.c_double(lo), ctypes.c_double(hi), self.s())
+        else:
+            call("cbct_clip", self.plan, _p(vol), ctypes.c_float(lo), ctypes.c_float(hi), self.s())
 
     def fill_volume(self, vol, value):
-        call("cbct_fill_volume", self.plan, _p(vol), ctypes.c_float(value), self.s())
+        if self.f64:
+            call("cbct_fill_volume_f64", self.plan, _p(vol), ctypes.c_double(value), self.s())
+        else:
+            call("cbct_fill_volume", self.plan, _p(vol), ctypes.c_float(value), self.s())
 
 
 def _as_internal_volume(op, vol) -> torch.Tensor:
@@ -250,7 +273,7 @@ class _JacobiChain(_Chain):
         if dmax <= 0:
             raise DegenerateOperatorError("normal-equation diagonal is identically zero")
         floored = torch.clamp(diag.double(), min=floor_frac * dmax)
-        scale = (1.0 / torch.sqrt(floored)).float()
+        scale = (1.0 / torch.sqrt(floored)).to(self.dev.dtype)
         # zero the scale on the guard slices so scaled volumes keep zero guards
         mask = torch.zeros_like(scale)
         self.dev.fill_volume(mask, 1.0)
@@ -295,7 +318,6 @@ class _TikhonovChain(_Chain):
         self.m = inner.m + inner.n
         self.n_phys = inner.n_phys
         self.m_phys = inner.m_phys + inner.n_phys
-        self._tmpT = torch.empty(self.n_phys, dtype=torch.float32, device=self.dev.device)
 
     def apply(self, x, out, norm2=False):
         mi = self.inner.m_phys
@@ -317,7 +339,7 @@ class _TikhonovChain(_Chain):
         return self.inner.x_of(z)
 
     def rhs(self, b):
-        out = torch.zeros(self.m_phys, dtype=torch.float32, device=self.dev.device)
+        out = torch.zeros(self.m_phys, dtype=self.dev.dtype, device=self.dev.device)
         out[: self.inner.m_phys] = self.inner.rhs(b)
         return out
 
@@ -353,7 +375,7 @@ def _check_inputs(op, b, cfg: SolverConfig, method: str) -> None:  # solvers.py:
 
 def _x0_internal(op, cfg: SolverConfig, dev: _Dev) -> torch.Tensor:
     if cfg.initial_x0 is None:
-        return torch.zeros(dev.vol_elems, dtype=torch.float32, device=dev.device)
+        return torch.zeros(dev.vol_elems, dtype=dev.dtype, device=dev.device)
     return _as_internal_volume(op, cfg.initial_x0).clone()
 
 
@@ -364,7 +386,7 @@ def _norm(dev: _Dev, v) -> float:
 def _final_volume(op, x_int, like):
     """Report the solution in the caller's container kind (numpy fp64 for host b)."""
     if isinstance(like, torch.Tensor) and getattr(like, "is_cuda", False):
-        return Volume(op.vol_geom, op.volume_from_internal(x_int, torch.float32))
+        return Volume(op.vol_geom, op.volume_from_internal(x_int, getattr(op, "dtype", torch.float32)))
     return Volume(op.vol_geom, hostcopy.to_host(op.volume_from_internal(x_int, torch.float64)))
 
 
@@ -392,12 +414,12 @@ class CglsRun:
         self.dev = dev = _Dev(op)
         self.chain = chain = _build_chain(op, cfg, dev)
         self.t0 = time.perf_counter()
-        self.x = _alloc(chain.n, chain.n_phys, dev.device)
+        self.x = _alloc(chain.n, chain.n_phys, dev.device, dev.dtype)
         self.x.copy_(chain.z_of(_x0_internal(op, cfg, dev)))
-        self.d = _alloc(chain.n, chain.n_phys, dev.device)
-        self.r = _alloc(chain.n, chain.n_phys, dev.device)
-        self.e = _alloc(chain.m, chain.m_phys, dev.device)
-        self.p = _alloc(chain.m, chain.m_phys, dev.device)
+        self.d = _alloc(chain.n, chain.n_phys, dev.device, dev.dtype)
+        self.r = _alloc(chain.n, chain.n_phys, dev.device, dev.dtype)
+        self.e = _alloc(chain.m, chain.m_phys, dev.device, dev.dtype)
+        self.p = _alloc(chain.m, chain.m_phys, dev.device, dev.dtype)
         self.history = []
         self.pending = 0.0  # deferred x += alpha*d
         self.i = 0
@@ -420,11 +442,15 @@ class CglsRun:
             return
         alpha = self.nr2_old / np2
         self.pending = alpha
-        self.nb = float(np.sqrt(_proj_update(dev, chain, e, p, alpha)))
+        self._set_norms(*_proj_update(dev, chain, e, p, alpha))
         self._record(0)
 
+    def _set_norms(self, head2, full2):
+        self.nb = float(np.sqrt(head2))       # history / final_discrepancy_norm (report_norm)
+        self.nb_full = float(np.sqrt(full2))  # the stop test (norm of the stacked e_b)
+
     def _stop_at_start(self):
-        self.nb = _norm(self.dev, self.chain.head(self.e))
+        self.nb = self.nb_full = _norm(self.dev, self.chain.head(self.e))
         self._record(0)
         self.done = self.breakdown = True
 
@@ -444,7 +470,7 @@ class CglsRun:
         self.history.append(ConvergenceRecord(i, time.perf_counter() - self.t0, self.rel(self.nb), true_e))
 
     def should_continue(self) -> bool:
-        return (not self.done) and self.rel(self.nb) > self.cfg.rel_discrepancy_tol and \
+        return (not self.done) and self.rel(self.nb_full) > self.cfg.rel_discrepancy_tol and \
             self.i < self.cfg.max_iterations
 
     def step(self, record: bool = True) -> bool:
@@ -464,7 +490,7 @@ class CglsRun:
             return False
         alpha = self.nr2_old / np2
         self.pending = alpha
-        self.nb = float(np.sqrt(_proj_update(dev, chain, self.e, self.p, alpha)))
+        self._set_norms(*_proj_update(dev, chain, self.e, self.p, alpha))
         self.i += 1
         if record:
             self._record(self.i)
@@ -475,7 +501,7 @@ class CglsRun:
         """The plain fused chain (no Jacobi/Tikhonov stacking) without true-discrepancy
         monitoring can run with every scalar on the device (``run_device``)."""
         c = self.chain
-        return type(c) is _Chain and c._fused and self.cfg.true_discrepancy_every <= 0
+        return type(c) is _Chain and c._fused and self.cfg.true_discrepancy_every <= 0 and not self.dev.f64
 
     def _device_scalars(self) -> torch.Tensor:
         """The fp64 scalar array of include/cbct.h cbct_cgls_scalars, loaded from the host state."""
@@ -536,7 +562,7 @@ class CglsRun:
         it = int(h[7])
         now = time.perf_counter() - self.t0
         for j in range(self._i0 + 1, it + 1):
-            self.nb = float(np.sqrt(h[16 + j]))
+            self.nb = self.nb_full = float(np.sqrt(h[16 + j]))  # plain chain: no stacked tail
             self.history.append(ConvergenceRecord(j, now, self.rel(self.nb), None))
         self.i = it
         if h[6] == 1.0:
@@ -568,12 +594,14 @@ _DEVICE_BATCH = 8
 
 
 def _proj_update(dev, chain, e, p, alpha):
-    """e -= alpha*p over the whole (possibly stacked) vector; returns ||head(e)||^2."""
+    """e -= alpha*p over the whole (possibly stacked) vector.  Returns (||head(e)||^2,
+    ||e||^2): the reference records the data-block norm (report_norm, solvers.py:152-155)
+    but stops on the full stacked norm (solvers.py:334, 339, 355)."""
     mo = chain.head(e).numel()
     nb2 = dev.axpby(-alpha, p[:mo], 1.0, e[:mo], norm2=True)
     if e.numel() > mo:
-        dev.axpby(-alpha, p[mo:], 1.0, e[mo:])
-    return nb2
+        return nb2, nb2 + dev.axpby(-alpha, p[mo:], 1.0, e[mo:], norm2=True)
+    return nb2, nb2
 
 
 def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
@@ -601,19 +629,19 @@ def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
         return SolverReport(_final_volume(op, chain.x_of(x), b.data), i, phibar, history,
                             getattr(op, "workers", 1), breakdown)
 
-    u = torch.empty(chain.m_phys, dtype=torch.float32, device=dev.device)
+    u = dev.empty(chain.m_phys)
     chain.apply(x, u)
     beta = float(np.sqrt(dev.sub(b_eff, u, u, norm2=True)))
     if beta == 0.0:
         record(0, 0.0)
         return finish(0, 0.0, True)
-    dev.axpby(0.0, None, 1.0 / beta, u)
-    v = torch.empty(chain.n_phys, dtype=torch.float32, device=dev.device)
+    dev.div(u, beta)
+    v = dev.empty(chain.n_phys)
     alpha = float(np.sqrt(chain.applyT(u, v, norm2=True)))
     if alpha == 0.0:
         record(0, rel(beta))
         return finish(0, beta, True)
-    dev.axpby(0.0, None, 1.0 / alpha, v)
+    dev.div(v, alpha)
     w = v.clone()
     phibar, rhobar = beta, alpha
     tmp_m = torch.empty_like(u)
@@ -625,11 +653,11 @@ def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
         chain.apply(v, tmp_m)
         beta = float(np.sqrt(dev.axpby(1.0, tmp_m, -alpha, u, norm2=True)))  # u = A v - alpha u
         if beta > 0.0:
-            dev.axpby(0.0, None, 1.0 / beta, u)
+            dev.div(u, beta)
             chain.applyT(u, tmp_n)
             alpha = float(np.sqrt(dev.axpby(1.0, tmp_n, -beta, v, norm2=True)))  # v = A^T u - beta v
             if alpha > 0.0:
-                dev.axpby(0.0, None, 1.0 / alpha, v)
+                dev.div(v, alpha)
         rho = float(np.hypot(rhobar, beta))
         c, s = rhobar / rho, beta / rho
         theta = s * alpha
@@ -662,8 +690,8 @@ def normal_spectral_radius(op, power_iterations: int = 10) -> float:
 
 
 def _spectral(op, dev, inv_row, iters):
-    proj = torch.empty(op.m, dtype=torch.float32, device=dev.device)
-    w = torch.empty(dev.vol_elems, dtype=torch.float32, device=dev.device)
+    proj = dev.empty(op.m)
+    w = dev.empty(dev.vol_elems)
     v = torch.empty_like(w)
     dev.fill_volume(v, 1.0)
     chain = _Chain(op, dev)
@@ -674,7 +702,7 @@ def _spectral(op, dev, inv_row, iters):
         if norm == 0.0:
             raise DegenerateOperatorError("operator never intersects the volume")
         v.copy_(w)
-        dev.axpby(0.0, None, 1.0 / norm, v)
+        dev.div(v, norm)
     chain.apply(v, proj)
     dev.mul(proj, inv_row, proj)
     chain.applyT(proj, w)
@@ -698,7 +726,7 @@ def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solver
         raise DegenerateOperatorError("operator never intersects the volume")
     inv_row = _inv_positive(row)
     if method == "sirt":
-        step_vec = (cfg.relaxation * _inv_positive(col)).float()
+        step_vec = (cfg.relaxation * _inv_positive(col)).to(dev.dtype)
         step = None
     else:
         step_vec = None
@@ -717,9 +745,9 @@ def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solver
     def record(i, e):
         history.append(ConvergenceRecord(i, time.perf_counter() - t0, e, e if _want_true(cfg, i) else None))
 
-    resid = torch.empty(op.m, dtype=torch.float32, device=dev.device)
+    resid = dev.empty(op.m)
     weighted = torch.empty_like(resid)
-    upd = torch.empty(dev.vol_elems, dtype=torch.float32, device=dev.device)
+    upd = dev.empty(dev.vol_elems)
     chain.apply(x, resid)
     e = rel(float(np.sqrt(dev.sub(b_int, resid, resid, norm2=True))))
     record(0, e)
