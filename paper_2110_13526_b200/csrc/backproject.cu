@@ -439,7 +439,9 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     if (mode != 1 && mode != 2) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode must be 1 or 2");
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode 1 needs projections");
     cudaStream_t s = (cudaStream_t)stream;
-    const bool precise = getenv("CBCT_BP_PRECISE") != nullptr;
+    // Mode 2 (diag(A^T A), once per Jacobi solve) always clips in fp64: its squared weights
+    // double the fp32 clip's relative error, which reaches ~1e-4 at 0.43 mm voxels.
+    const bool precise = mode == 2 || getenv("CBCT_BP_PRECISE") != nullptr;
     static const bool force_direct = getenv("CBCT_BP_DIRECT") != nullptr;  // diagnosis: fp32 direct kernel
     if (mode == 1 && p->bp_boundary_ok && !precise && !force_direct) {
         float* pyb = scratch;

@@ -1,0 +1,198 @@
+"""Solver-iterate parity at the BASELINE configs against iterates the REFERENCE computed.
+
+north_star: "CGLS iterate relative L2 difference <= 1e-3 after the named iteration count".
+The goldens were written by the reference itself (cbctkit 0.1.0, fp64, workers = 8) in the
+build container (tests/golden/make_golden_configs.py, make_golden_trajectory.py):
+
+* ``config34_subset``  -- BASELINE configs 3/4 on a reference-valid subset:
+  the 512^3 / 616x480 geometry at its own 0.43 mm voxels and 0.616 mm pixels, a 32-slice
+  central z slab and every 8th of the 720 views (full angular coverage).  CGLS-40
+  (solvers.py:269-358), LSQR-40 with Jacobi preconditioning (config 4's solver,
+  solvers.py:158-193, 361-459) and PSIRT-40 (solvers.py:505-569), plus the CGLS / LSQR-J
+  iterates after 10, 20 and 30 iterations.
+* ``config2_trajectory`` (when present) -- BASELINE config 2 in full: 256^3, 360 views of
+  512x384, CGLS-40 with snapshots at 10/20/30/40.
+
+Both precisions of the operator are held to the north-star bar: the fp32 fast path and the
+fp64 reference-precision path (``precision="f64"``, csrc/f64.cu).  The goldens also carry the
+reference's own reproducibility floor (the same solve with workers = 5, which only changes the
+backprojector's summation order): the fp64 path is additionally held to 10x that floor, or 1e-9
+where the floor is below fp64 resolution.
+
+b is the inverse-crime data of the reference tests (conftest.py:59-66): the fp64 oracle's
+A phantom, rounded to fp32 so both sides see the same fp32-representable b; its strided sample
+must equal the golden's bit for bit (proof that this test rebuilt the reference's b).
+"""
+
+import numpy as np
+import pytest
+
+from _helpers import geom_from_golden, load_golden, rel_l2
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-3   # north star: iterate rel-L2
+H_TOL = 1e-3   # history records, relative
+
+
+@pytest.fixture(scope="module")
+def subset():
+    d = load_golden("config34_subset")
+    t = load_golden("config34_subset_trajectory")
+    vg, tr = geom_from_golden(d)
+    ref = O.OracleOperator(vg, tr)
+    b = ref.project(O.shepp_logan_phantom(vg)).astype(np.float32).astype(np.float64)
+    assert np.array_equal(b[:: int(d["b_stride"])], d["b_sample"]), "b differs from the reference's b"
+    return d, t, vg, tr, b
+
+
+_OPS = {}
+
+
+def _op(vg, tr, precision):
+    import paper_2110_13526_b200 as P
+
+    key = (precision, vg.nx, vg.nz, tr.n_views)
+    if key not in _OPS:
+        _OPS.clear()
+        _OPS[key] = P.CbctOperator(vg, tr, precision=precision)
+    return _OPS[key]
+
+
+def _solve(op, tr, b, method, K, **kw):
+    import paper_2110_13526_b200 as P
+
+    rep = P.solve(op, P.ProjectionStack(tr, b), P.SolverConfig(method=method, max_iterations=K, **kw))
+    return rep, np.array([r.rel_discrepancy for r in rep.history])
+
+
+def _floor_bar(t, key, K):
+    f = t.get(f"{key}_x{K}_floor")
+    return None if f is None else max(10.0 * float(f), 1e-9)
+
+
+_SOLVERS = [("cgls40", "cgls", {}), ("lsqrj40", "lsqr", {"jacobi_precondition": True}), ("psirt40", "psirt", {})]
+
+
+@pytest.mark.parametrize("key,method,kw", _SOLVERS)
+def test_config34_subset_40_iterations_f64(subset, key, method, kw):
+    """The north-star bar at the named iteration count (40) on the reference-precision path:
+    iterate rel-L2 <= 1e-3 (measured: CGLS 5.4e-5, LSQR-J 3.4e-4, PSIRT 2e-15; the reference's
+    own floor is 2.3e-5 / 1.6e-5), the history to 1e-12 while the Krylov recurrences are still
+    in their rounding-stable phase (records 0-20) and the final discrepancy to 1e-2."""
+    d, t, vg, tr, b = subset
+    op = _op(vg, tr, "f64")
+    rep, h = _solve(op, tr, b, method, 40, **kw)
+    assert rep.iterations == int(d[f"{key}_iterations"])
+    hr = d[f"{key}_hist"]
+    assert h.shape == hr.shape
+    assert float(np.abs(h[:21] / hr[:21] - 1.0).max()) <= 1e-12
+    assert abs(h[-1] / hr[-1] - 1.0) <= 1e-2
+    rel = rel_l2(rep.final_x.data[:: int(d["x_stride"])], d[f"{key}_x_sample"])
+    assert abs(np.linalg.norm(rep.final_x.data) / float(d[f"{key}_x_norm"]) - 1.0) <= X_TOL
+    assert rel <= X_TOL, (key, "iterate", rel)
+
+
+def test_config34_subset_psirt40_f32(subset):
+    """PSIRT is not a Krylov recurrence: the fp32 fast path follows the reference's 40
+    iterations (measured 2e-6 iterate, 7e-6 history)."""
+    d, t, vg, tr, b = subset
+    rep, h = _solve(_op(vg, tr, "f32"), tr, b, "psirt", 40)
+    assert float(np.abs(h / d["psirt40_hist"] - 1.0).max()) <= H_TOL
+    assert rel_l2(rep.final_x.data[:: int(d["x_stride"])], d["psirt40_x_sample"]) <= X_TOL
+
+
+@pytest.mark.parametrize("key,method,kw", _SOLVERS[:2])
+def test_config34_subset_krylov40_f32_floor(subset, key, method, kw):
+    """What fp32 storage does to a 40-iteration Krylov iterate at this conditioning (a
+    regression guard, not the parity bar).  The reference's own CGLS iterate moves by 5e-16 /
+    4e-12 / 4e-7 / 2e-5 at K = 10/20/30/40 when only its backprojector's summation order
+    changes: rounding perturbations grow ~5e10x over these 30 iterations (loss of
+    orthogonality).  tools/precision_experiment.py (profiles/precision_r2.md) shows that ANY
+    fp32 rounding crosses 1e-3 by K = 40 -- even exact fp64 arithmetic whose operator input and
+    output are merely rounded to fp32 (5.0e-3), or fp64 vectors around the fp32 kernels
+    (8.1e-3).  Hence the fp64 path above is the parity path; the fp32 path holds the iterate to
+    1e-3 through K = 10 (next test) and reaches a discrepancy within 20% of the reference's."""
+    d, t, vg, tr, b = subset
+    rep, h = _solve(_op(vg, tr, "f32"), tr, b, method, 40, **kw)
+    assert float(np.abs(h[:11] / d[f"{key}_hist"][:11] - 1.0).max()) <= 1e-6
+    assert h[-1] <= 1.2 * d[f"{key}_hist"][-1]
+    assert rel_l2(rep.final_x.data[:: int(d["x_stride"])], d[f"{key}_x_sample"]) <= 1.5e-2
+
+
+@pytest.mark.parametrize("precision,K", [("f32", 10), ("f64", 10), ("f64", 20), ("f64", 30)])
+@pytest.mark.parametrize("tk,method,kw", [("cgls", "cgls", {}), ("lsqrj", "lsqr", {"jacobi_precondition": True})])
+def test_config34_subset_trajectory(subset, precision, K, tk, method, kw):
+    """Snapshots of the reference's CGLS / LSQR-J iterate after K iterations.  fp64: held to
+    the reference's own reproducibility floor (x10, and no tighter than the fp32-stored golden
+    sample resolves) through K = 20, and to 1e-3 at K = 30 for CGLS (measured 1.3e-6).  LSQR-J
+    at K = 30 sits at the peak of its rounding-amplification transient (the reference's own
+    history deviation grows 1e3x per two records there) and is only held at K = 40 (previous
+    tests).  fp32: K = 10."""
+    if (tk, K) == ("lsqrj", 30):
+        pytest.skip("LSQR-J K=30 is mid-transient; the named count (40) is asserted above")
+    d, t, vg, tr, b = subset
+    op = _op(vg, tr, precision)
+    rep, h = _solve(op, tr, b, method, K, **kw)
+    hr = t[f"{tk}_w8_hist"][: K + 1]
+    assert float(np.abs(h / hr - 1.0).max()) <= (1e-6 if K <= 20 else H_TOL)
+    rel = rel_l2(rep.final_x.data[:: int(t["x_stride"])], t[f"{tk}_w8_x{K}_sample"])
+    assert rel <= X_TOL, (precision, tk, K, rel)
+    if precision == "f64" and K <= 20:
+        assert rel <= max(_floor_bar(t, tk, K), 2e-7), (tk, K, rel)  # fp32-stored golden sample: 6e-8/voxel
+
+
+def test_config34_subset_normal_diagonal(subset):
+    """diag(A^T A) (operator.py:353-362) at config 3/4's 0.43 mm voxels: the Jacobi scale of
+    config 4's LSQR, on the subset's 90 views (the fp64 z clip of mode 2)."""
+    from _helpers import max_rel
+
+    d, t, vg, tr, b = subset
+    ref = O.OracleOperator(vg, tr)
+    for precision in ("f32", "f64"):
+        op = _op(vg, tr, precision)
+        got = op.normal_diagonal().data
+        want = ref.normal_diagonal()
+        assert max_rel(got, want) <= 1e-4, (precision, max_rel(got, want))
+        assert rel_l2(got, want) <= 1e-5, (precision, rel_l2(got, want))
+
+
+def _config2():
+    import pathlib
+
+    p = pathlib.Path(__file__).resolve().parent / "golden" / "config2_trajectory.npz"
+    return load_golden("config2_trajectory") if p.exists() else None
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_config2_cgls40_full(precision):
+    """BASELINE config 2 in full (256^3, 360 views of 512x384): the reference's CGLS iterate
+    after 10/20/40 iterations.  fp64 path: 1e-3 at K = 20 and at the named count 40; fp32 path:
+    1e-3 at K = 10, and at K = 40 the fp32 floor of the subset test above."""
+    t = _config2()
+    if t is None:
+        pytest.skip("config2_trajectory.npz not generated")
+    import paper_2110_13526_b200 as P
+
+    vg, tr = geom_from_golden(t)
+    op = P.CbctOperator(vg, tr, precision=precision)
+    # inverse-crime b: the fp64 projector is bitwise the reference's (operator.py:190-206),
+    # rounded to fp32 exactly as the golden script did
+    truth = P.Volume(vg, O.shepp_logan_phantom(vg))
+    bop = op if precision == "f64" else P.CbctOperator(vg, tr, precision="f64")
+    b = bop.project(truth).data.astype(np.float32).astype(np.float64)
+    del bop
+    assert np.array_equal(b[:: int(t["b_stride"])], t["b_sample"]), "b differs from the reference's b"
+    for K in ((20, 40) if precision == "f64" else (10, 40)):
+        rep, h = _solve(op, tr, b, "cgls", K)
+        hr = t["cgls_w8_hist"][: K + 1]
+        rel = rel_l2(rep.final_x.data[:: int(t["x_stride"])], t[f"cgls_w8_x{K}_sample"])
+        if precision == "f64" or K <= 10:
+            assert float(np.abs(h[:11] / hr[:11] - 1.0).max()) <= 1e-6
+            assert rel <= X_TOL, (precision, K, rel)
+        else:
+            assert h[-1] <= 1.2 * hr[-1]
+            assert rel <= 1.5e-2, (precision, K, rel)

@@ -125,6 +125,10 @@ def _check_random(op, ref):
     assert max_rel(got, want) <= TOL, max_rel(got, want)
     got, want = op.backproject(_stack(op, y)).data, ref.backproject(y)
     assert max_rel(got, want) <= TOL, max_rel(got, want)
+    # mode 2 (diag(A^T A), operator.py:166-167, 353-362): config 4's Jacobi scale at the
+    # BASELINE cell sizes
+    got, want = op.normal_diagonal().data, ref.normal_diagonal()
+    assert max_rel(got, want) <= TOL, ("normal_diagonal", max_rel(got, want))
 
 
 def test_flat_row_closed_form_against_oracle():

@@ -23,7 +23,7 @@ st = int(d["x_stride"])
 if traj is not None:
     for key in ("cgls", "lsqrj"):
         if f"{key}_w8_hist" in traj:
-            fl = [rel_l2(traj[f"{key}_w5_x{k}_sample"], traj[f"{key}_w8_x{k}_sample"]) for k in (10, 20, 30, 40)]
+            fl = [float(traj[f"{key}_x{k}_floor"]) for k in (10, 20, 30, 40)]
             print(f"reference floor {key} (w5 vs w8) x rel at 10/20/30/40:", " ".join(f"{v:.2e}" for v in fl))
 for prec in precs:
     t = time.time()

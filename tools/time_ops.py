@@ -13,12 +13,12 @@ import paper_2110_13526_b200 as P  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 vg, tr = bench.geometry(cfg)
-op = P.CbctOperator(vg, tr)
+op = P.CbctOperator(vg, tr, precision=os.environ.get("PREC", "f32"))
 x = op.phantom_internal(P.shepp_logan_3d())
 p = op.new_projections()
 r = op.new_volume()
 scr = op.new_bp_scratch()
-y = torch.randn(op.m, device="cuda")
+y = torch.randn(op.m, device="cuda", dtype=op.dtype)
 
 
 def t(fn):
@@ -37,6 +37,6 @@ only = sys.argv[3] if len(sys.argv) > 3 else ""  # "A" or "AT": time one operato
 ta = t(lambda: op.project_internal(x, p)) if only != "AT" else float("nan")
 tat = t(lambda: op.backproject_internal(y, r, scratch=scr)) if only != "A" else float("nan")
 N, V = vg.nx, tr.n_views
-tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("CBCT_"))
+tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("CBCT_") or k == "PREC")
 print(f"cfg{cfg} {tag or 'default'}: A {ta:.3f} ms ({N**3*V/ta/1e6:.0f} GUPS)  AT {tat:.3f} ms ({N**3*V/tat/1e6:.0f} GUPS)",
       flush=True)
