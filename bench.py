@@ -1,18 +1,20 @@
-"""Benchmark: CGLS iterations/s and GUPS of A / A^T on B200 (BASELINE.json metric).
+"""Benchmark: solver iterations/s and GUPS of A / A^T on B200 (BASELINE.json metric).
 
-Default workload (N=1): BASELINE config 2 -- 3-D Shepp-Logan 256^3, 360 views of a
-512x384 detector, CGLS (SURVEY.md 8(d) geometry rule: SID 749, SDD 1198, 0.86 mm
-voxels, 0.741 mm pixels).  A "step" is one steady-state CGLS loop iteration
-(solvers.py:339-357): A^T (+||r||^2), fused volume update, A (+||p||^2), fused
-projection update (+||e||^2).  Inputs stay resident in HBM; the working set
-(67 MB volume + 3 x 283 MB projection vectors) exceeds the 126 MB L2, so no
-explicit flush is needed between steps.
+Default workload (N=1): BASELINE config 3 -- the north-star size, 3-D Shepp-Logan 512^3,
+720 views of a 616x480 detector, CGLS (SURVEY.md 8(d) geometry rule: SID 749, SDD 1198,
+0.43 mm voxels, 0.616 mm pixels).  A "step" is one steady-state solver loop iteration; for
+CGLS (solvers.py:339-357): A^T (+||r||^2), fused volume update, A (+||p||^2), fused
+projection update (+||e||^2).  ``--config 4`` (or ``--solver lsqr-jacobi``) times LSQR with
+Jacobi preconditioning, ``--solver psirt`` PSIRT; ``--precision f64`` the reference-precision
+path.  Inputs stay resident in HBM; the working set (0.55 GB volume + 3 x 0.85 GB projection
+vectors at config 3) exceeds the 126 MB L2, so no explicit flush is needed between steps.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--solver S]
+                    [--precision f32|f64] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
-algorithm's CPU restatement (oracle/, C + OpenMP, all host threads) on a bounded
-view sample of the same workload.
+algorithm's CPU restatement (oracle/, C + OpenMP, all host threads) on bounded
+view samples of the same workload.
 """
 
 from __future__ import annotations
@@ -122,22 +124,19 @@ def committed_traffic(cfg: int) -> dict:
 
 
 # ------------------------------------------------------------------ CPU legs --
-def cpu_sample(cfg: int, nviews: int = None, threads: int = 0):
-    """Reference algorithm (oracle port, C+OpenMP, fp64) on a contiguous view sample of
-    the workload: returns seconds for one A and one A^T scaled to all views, plus the
-    vector-update time, i.e. the CPU time of one CGLS iteration."""
+def _oracle_ops(cfg, k, threads):
     from oracle import oracle as O
     from paper_2110_13526_b200.geometry import make_circular_trajectory
 
     vg, tr = geometry(cfg)
-    V = tr.n_views
-    threads_avail = int(O.lib().oracle_max_threads()) if threads < 1 else threads
-    # enough views that the worker-parallel backprojector uses every host thread
-    k = nviews or max(1, min(V, max(threads_avail, {1: 90, 2: 6, 3: 2, 4: 2, 5: 1}[cfg])))
-    sub = make_circular_trajectory(tr.sid, tr.sdd, k, 0.0, k * tr.angular_span / V, tr.detector)
-    # backprojector workers as the reference deals them (operator.py:219-220), capped so the
-    # private accumulators stay small (BASELINE.md 4.1)
-    workers = max(1, min(threads_avail, k, 64))
+    sub = make_circular_trajectory(tr.sid, tr.sdd, k, 0.0, k * tr.angular_span / tr.n_views, tr.detector)
+    return O, vg, tr, sub
+
+
+def cpu_time_views(cfg: int, k: int, workers: int, threads: int = 0):
+    """One A and one A^T of the reference algorithm (oracle port, C + OpenMP, fp64) on the first
+    k views of the workload; returns (t_A, t_AT) in seconds."""
+    O, vg, tr, sub = _oracle_ops(cfg, k, threads)
     op = O.OracleOperator(vg, sub, workers=workers, threads=threads)
     x = np.random.default_rng(0).random(op.n)
     y = np.random.default_rng(1).standard_normal(op.m)
@@ -147,8 +146,12 @@ def cpu_sample(cfg: int, nviews: int = None, threads: int = 0):
     t0 = time.perf_counter()
     op.backproject(y)
     tat = time.perf_counter() - t0
-    scale = V / k
-    # vector work of one CGLS iteration in fp64 numpy (solvers.py:340-355), full size
+    return ta, tat
+
+
+def cpu_vector_time(cfg: int):
+    """Vector work of one CGLS iteration in fp64 numpy (solvers.py:340-355), full size."""
+    vg, tr = geometry(cfg)
     n, m = vg.nx * vg.ny * vg.nz, tr.n_rays
     xv, dv, rv = np.zeros(n), np.ones(n), np.ones(n)
     t0 = time.perf_counter()
@@ -164,34 +167,90 @@ def cpu_sample(cfg: int, nviews: int = None, threads: int = 0):
     ev -= 0.1 * pv
     _ = float(np.linalg.norm(ev))
     tv_m = time.perf_counter() - t0
-    del ev, pv
-    t_iter = ta * scale + tat * scale + tv_n + tv_m
-    return {"t_A": ta * scale, "t_AT": tat * scale, "t_vec": tv_n + tv_m, "t_iter": t_iter,
-            "views_sampled": k, "threads": int(O.lib().oracle_max_threads()) if threads < 1 else threads}
+    return tv_n + tv_m
+
+
+def cpu_views(cfg: int, threads: int) -> int:
+    """Sample size: enough views that the worker-parallel backprojector uses every host thread
+    (its parallelism is min(workers, threads), operator.py:219), at most the whole trajectory."""
+    V = CONFIGS[cfg][1]
+    return max(1, min(V, threads, 32))
+
+
+def cpu_extrapolate(cfg: int, k: int, t1, t2):
+    """Per-view slope and fixed cost from samples at k and 2k views (same worker count):
+    t(v) = F + v s  ->  full = F + V s.  The A^T fixed cost (the W private accumulators'
+    allocation and their serial merge, operator.py:222-233) is counted once, not V/k times."""
+    V = CONFIGS[cfg][1]
+    out = {}
+    for name, a, b in (("t_A", t1[0], t2[0]), ("t_AT", t1[1], t2[1])):
+        slope = max((b - a) / k, 0.0)
+        fixed = max(a - k * slope, 0.0)
+        if slope == 0.0:  # timing noise: fall back to proportional scaling
+            slope, fixed = a / k, 0.0
+        out[name] = fixed + V * slope
+        out[name + "_fixed"] = fixed
+    return out
+
+
+def cpu_sample(cfg: int, threads: int = 0):
+    """CPU time of one CGLS iteration of the reference algorithm (one A + one A^T + the vector
+    updates) on this host, extrapolated from two view samples (k and 2k views)."""
+    from oracle import oracle as O
+
+    threads = int(O.lib().oracle_max_threads()) if threads < 1 else threads
+    V = CONFIGS[cfg][1]
+    k = cpu_views(cfg, threads)
+    workers = min(threads, k)
+    t1 = cpu_time_views(cfg, k, workers, threads)
+    if 2 * k <= V:
+        t2 = cpu_time_views(cfg, 2 * k, workers, threads)
+        ex = cpu_extrapolate(cfg, k, t1, t2)
+        how = f"A and A^T timed on {k} and {2 * k} of {V} views, per-view slope x {V} + fixed cost"
+    else:
+        ex = {"t_A": t1[0] * V / k, "t_AT": t1[1] * V / k, "t_A_fixed": 0.0, "t_AT_fixed": 0.0}
+        how = f"A and A^T on all {V} views"
+    tv = cpu_vector_time(cfg)
+    return {**ex, "t_vec": tv, "t_iter": ex["t_A"] + ex["t_AT"] + tv, "views_sampled": k, "workers": workers,
+            "threads": threads, "sample": how + "; vector updates at full size (numpy fp64)", "extrapolated": k < V}
 
 
 def run_reference(args, cfg, rank, world):
+    """The reference arm: the reference algorithm's CPU implementation (oracle port, all host
+    threads) on rank 0.  One step = one A + one A^T on a k-view sample of the workload; after the
+    K timed steps one 2k-view sample gives the per-view slope, and the CGLS iteration time is
+    extrapolated to all views (cpu_extrapolate)."""
     if rank != 0:
         return 0
-    samples = []
-    for _ in range(args.warmup):
-        cpu_sample(cfg)
-    for _ in range(args.steps):
-        samples.append(cpu_sample(cfg))
-    t_iter = float(np.median([s["t_iter"] for s in samples]))
+    from oracle import oracle as O
+
+    threads = int(O.lib().oracle_max_threads())
     N, V, nu, nv, solver, K = CONFIGS[cfg]
-    s0 = samples[0]
+    k = cpu_views(cfg, threads)
+    workers = min(threads, k)
+    for _ in range(args.warmup):
+        cpu_time_views(cfg, k, workers)
+    samples = [cpu_time_views(cfg, k, workers) for _ in range(args.steps)]
+    t1 = (float(np.median([s[0] for s in samples])), float(np.median([s[1] for s in samples])))
+    if 2 * k <= V:
+        ex = cpu_extrapolate(cfg, k, t1, cpu_time_views(cfg, 2 * k, workers))
+    else:
+        ex = {"t_A": t1[0] * V / k, "t_AT": t1[1] * V / k, "t_A_fixed": 0.0, "t_AT_fixed": 0.0}
+    t_iter = ex["t_A"] + ex["t_AT"] + cpu_vector_time(cfg)
     val = 1.0 / t_iter
+    sample = (f"A and A^T of the reference algorithm on {k} of {V} views (median of {args.steps} steps) and once "
+              f"on {2 * k} views; iteration = fixed cost + {V} x per-view slope; workers {workers}, "
+              f"{threads} OpenMP threads; vector updates at full size (numpy fp64)")
     line = {
         "impl": "reference", "metric": "CGLS iterations/sec", "value": val, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_iter * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, {solver}",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
                    "parallelism": "cpu-openmp"},
-        "gups_A": N ** 3 * V / s0["t_A"] / 1e9, "gups_AT": N ** 3 * V / s0["t_AT"] / 1e9,
-        "cpu_baseline": {"value": val, "unit": "it/s", "cores": s0["threads"], "kind": "port",
-                         "sample": f"A and A^T on {s0['views_sampled']} of {V} views, scaled by views; "
-                                   f"vector updates at full size (numpy fp64)"},
+        "gups_A": N ** 3 * V / ex["t_A"] / 1e9, "gups_AT": N ** 3 * V / ex["t_AT"] / 1e9,
+        "t_A_s": ex["t_A"], "t_AT_s": ex["t_AT"], "t_AT_fixed_s": ex["t_AT_fixed"],
+        "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port", "sample": sample,
+                         "extrapolated": True},
         "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,47 +258,85 @@ def run_reference(args, cfg, rank, world):
 
 
 # ------------------------------------------------------------------ GPU leg --
+SOLVER_METHOD = {"cgls": ("cgls", {}), "lsqr-jacobi": ("lsqr", {"jacobi_precondition": True}), "psirt": ("psirt", {})}
+SOLVER_NAME = {"cgls": "CGLS", "lsqr-jacobi": "LSQR+Jacobi", "psirt": "PSIRT"}
+
+
+def _new_run(P, op, b, solver, iters):
+    from paper_2110_13526_b200.solvers import ClassicalRun, CglsRun, LsqrRun, SolverConfig
+
+    method, kw = SOLVER_METHOD[solver]
+    cfg = SolverConfig(method=method, max_iterations=iters, **kw)
+    if method == "cgls":
+        return CglsRun(op, b, cfg)
+    if method == "lsqr":
+        return LsqrRun(op, b, cfg)
+    return ClassicalRun(op, b, cfg, method)
+
+
 def run_ours(args, cfg, rank, world, local_rank):
-    """N = 1: the single-GPU CGLS step (N > 1 goes through run_sharded)."""
+    """N = 1: one steady-state solver iteration per step (N > 1 goes through run_sharded)."""
     import torch
 
     import paper_2110_13526_b200 as P
     from paper_2110_13526_b200 import _lib
-    from paper_2110_13526_b200.solvers import CglsRun, SolverConfig
+    from paper_2110_13526_b200.solvers import SolverConfig
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    N, V, nu, nv, solver, K = CONFIGS[cfg]
+    N, V, nu, nv, _, K = CONFIGS[cfg]
+    solver = args.solver or CONFIGS[cfg][4]
+    sname = SOLVER_NAME[solver]
     vg, tr = geometry(cfg)
     t_setup = time.perf_counter()
-    op = P.CbctOperator(vg, tr, device=dev)
+    op = P.CbctOperator(vg, tr, device=dev, precision=args.precision)
     x_int = op.phantom_internal(P.shepp_logan_3d())  # device voxelizer (bit-identical to generate_phantom)
     b_int = op.new_projections()
-    op.project_internal(x_int, b_int)  # inverse crime b = A phantom (fp32, device)
+    op.project_internal(x_int, b_int)  # inverse crime b = A phantom (device)
+    del x_int
     b = P.operator.InternalProjections(tr, b_int)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
     steps, warmup = args.steps, args.warmup
-    scfg = SolverConfig(method="cgls", max_iterations=steps + warmup + 1)
-    run = CglsRun(op, b, scfg)
     stream = torch.cuda.current_stream(dev)
-
-    # the CGLS loop runs device-resident (scalars and stop tests on the GPU, no host round trip per
-    # iteration) as replays of one captured CUDA graph of the iteration (solvers.CglsRun.run_device)
-    run.run_device(warmup, graph=True)  # warm-up (captures the graph on its first call)
-    torch.cuda.synchronize()
+    run = _new_run(P, op, b, solver, steps + warmup + 1)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        start.record(stream)
-        run.run_device(steps, graph=True, collect=False)
-        end.record(stream)
+    device_loop = solver == "cgls" and run.device_capable()
+    if device_loop:
+        # the CGLS loop runs device-resident (scalars and stop tests on the GPU, no host round trip per
+        # iteration) as replays of one captured CUDA graph of the iteration (solvers.CglsRun.run_device)
+        run.run_device(warmup, graph=True)  # warm-up (captures the graph on its first call)
         torch.cuda.synchronize()
-    run.collect()
-    assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
-    launches = steps * run.graph_launches  # libcbct kernels per replayed iteration x replays
+        with ClockSampler(local_rank) as clk:
+            start.record(stream)
+            run.run_device(steps, graph=True, collect=False)
+            end.record(stream)
+            torch.cuda.synchronize()
+        run.collect()
+        assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
+        launches = steps * run.graph_launches  # libcbct kernels per replayed iteration x replays
+        loop = "device-resident CGLS, CUDA-graph replay per iteration"
+    else:
+        # host-driven loop (the reference's scalar recurrences on the host, fp64): each step is one
+        # full iteration including its blocking norm reads
+        for _ in range(warmup):
+            run.step()
+        torch.cuda.synchronize()
+        n0 = _lib.lib().cbct_launch_count()
+        with ClockSampler(local_rank) as clk:
+            start.record(stream)
+            for _ in range(steps):
+                run.step()
+            end.record(stream)
+            torch.cuda.synchronize()
+        launches = _lib.lib().cbct_launch_count() - n0
+        loop = f"host-driven {sname} loop ({args.precision})"
     ms = start.elapsed_time(end)
     # kernel-only durations: CUDA events tight around the launches on this stream
     scratch = op.new_bp_scratch()
+    vol_a, proj_a = op.new_volume(), op.new_projections()
+    vol_a.copy_(run.x if hasattr(run, "x") else vol_a)
+    proj_a.copy_(b_int)
 
     def kernel_ms(fn, reps=5):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -252,31 +349,41 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         return s.elapsed_time(e) / reps
 
-    t_a = kernel_ms(lambda: op.project_internal(run.d, run.p))
-    t_at = kernel_ms(lambda: op.backproject_internal(run.e, run.r, scratch=scratch))
+    reps = 5 if args.precision == "f32" else 2
+    out_p, out_v = op.new_projections(), op.new_volume()
+    t_a = kernel_ms(lambda: op.project_internal(vol_a, out_p), reps)
+    t_at = kernel_ms(lambda: op.backproject_internal(proj_a, out_v, scratch=scratch), reps)
+    del out_p, out_v, vol_a, proj_a
     ms_step = ms / steps
     value = 1e3 / ms_step
+    e_last = run.history[-1].rel_discrepancy if run.history else None
+    del run
+    torch.cuda.empty_cache()
 
-    # end-to-end through the public API: host fp64 b in, host x out, full solve
+    # end to end through the public API: host fp64 b in, host x out, the full solve (setup included)
     b_host = op.proj_from_internal(b_int, torch.float64).cpu().numpy()
     e2e_k = max(steps, 5)
     bstack = P.ProjectionStack(tr, b_host)
+    method, kw = SOLVER_METHOD[solver]
+    scfg = SolverConfig(method=method, max_iterations=e2e_k, **kw)
     t_solves = []
-    # one untimed solve first: the pinned staging buffers and copy threads are created on first use
-    P.cgls(op, bstack, SolverConfig(method="cgls", max_iterations=e2e_k))
-    for _ in range(3):  # median of 3 solves (~0.56 s each at config 2)
+    n_solves = 3 if args.precision == "f32" else 1
+    P.solve(op, bstack, scfg)  # untimed: the pinned staging buffers and copy threads are created on first use
+    for _ in range(n_solves):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = P.cgls(op, bstack, SolverConfig(method="cgls", max_iterations=e2e_k))
+        rep = P.solve(op, bstack, scfg)
         torch.cuda.synchronize()
         t_solves.append(time.perf_counter() - t0)
     t_e2e = float(np.median(t_solves))
     e2e = {"value": rep.iterations / t_e2e, "unit": "it/s",
            "h2d_bytes_per_step": int(op.m * 4 / e2e_k), "d2h_bytes_per_step": int((op.n * 8 + 24 * e2e_k) / e2e_k),
-           "note": f"cgls() on host fp64 ProjectionStack, K={e2e_k}, incl. pre-loop (2 A + 1 A^T) and the "
-                   f"pinned-staged host copies (hostcopy.py: b narrowed to fp32 on the host, x returned in fp64); "
-                   f"one untimed warm-up solve; "
-                   f"median of 3 solves ({', '.join(f'{1e3 * t:.0f}' for t in t_solves)} ms)"}
+           "note": f"{method}() on a host fp64 ProjectionStack, K={e2e_k}, including its setup "
+                   f"({'pre-loop 2 A + 1 A^T' if method == 'cgls' else 'normal_diagonal + pre-loop' if kw else 'pre-loop' if method == 'lsqr' else 'row/col sums + 11-step spectral radius'}) "
+                   f"and the pinned-staged host copies (hostcopy.py: b narrowed to the operator precision on the "
+                   f"host, x returned in fp64); one untimed warm-up solve; median of {n_solves} solves "
+                   f"({', '.join(f'{1e3 * t:.0f}' for t in t_solves)} ms)"}
+    del bstack, b_host
 
     peaks = measured_peaks()
     clocks = clk.summary()
@@ -285,13 +392,16 @@ def run_ours(args, cfg, rank, world, local_rank):
     nnz = NNZ[cfg]
     dom, t_dom = ("A^T", t_at) if t_at >= t_a else ("A", t_a)
     achieved = SLOTS_PER_NNZ * nnz / (t_dom * 1e-3)
-    kname = {"A^T": "k_bp_boundary", "A": "k_project_q"}[dom]
-    traffic = committed_traffic(cfg)
+    f32 = args.precision == "f32"
+    kname = {"A^T": "k_bp_boundary" if f32 else "k_bp64", "A": "k_project_q" if f32 else "k_project64"}[dom]
+    traffic = committed_traffic(cfg) if f32 else {}
     roof = {"bound": "issue", "kernel": f"{dom} ({kname})",
             "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
             "traffic": traffic.get(kname),
-            "traffic_unit": "B per operator application (DRAM read + write, ncu; A^T summed over its view-batch launches)",
+            "traffic_unit": "B per operator application (DRAM read + write, ncu --set full of this build; A^T "
+                            "summed over its view-batch launches)",
             "traffic_A": traffic.get("k_project_q"),
+            "traffic_source": traffic.get("source"),
             # the HBM view of the same kernel: measured DRAM bytes per application over the live time,
             # against MEASURED_PEAKS.json hbm_gbs (shows the kernel is not HBM-bound)
             "hbm_gbs": (traffic[kname] / (t_dom * 1e-3) / 1e9) if traffic.get(kname) else None,
@@ -300,8 +410,6 @@ def run_ours(args, cfg, rank, world, local_rank):
             if traffic.get(kname) and peaks.get("hbm_gbs") else None,
             "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
                           f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
-            # what ncu says binds each kernel (committed capture of the same build): A^T runs the L1/TEX
-            # data path near its peak on the z-row gathers, A is issue / barrier bound
             "ncu_utilisation": {k: v for k, v in traffic.get("ncu_utilisation", {}).items() if k != "source"} or None,
             "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
             "frac_AT": SLOTS_PER_NNZ * nnz / (t_at * 1e-3) / peak_slots}
@@ -309,23 +417,24 @@ def run_ours(args, cfg, rank, world, local_rank):
     if rank == 0 and not args.no_cpu:
         s = cpu_sample(cfg)
         cpu = {"value": 1.0 / s["t_iter"], "unit": "it/s", "cores": s["threads"], "kind": "port",
-               "sample": f"oracle A+A^T on {s['views_sampled']}/{V} views scaled to all views + full-size numpy "
-                         f"vector updates; t_A {s['t_A']:.2f}s t_AT {s['t_AT']:.2f}s"}
+               "sample": f"{s['sample']}; t_A {s['t_A']:.1f}s t_AT {s['t_AT']:.1f}s (fixed {s['t_AT_fixed']:.2f}s) "
+                         f"-> one CGLS iteration of the reference algorithm",
+               "extrapolated": s["extrapolated"], "workers": s["workers"]}
     line = {
-        "metric": "CGLS iterations/sec", "value": value, "unit": "it/s", "n_gpus": world, "steps": steps,
+        "metric": f"{sname} iterations/sec", "value": value, "unit": "it/s", "n_gpus": world, "steps": steps,
         "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
-                   "parallelism": "single",
+        "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, {sname} step",
+                   "solver": solver, "precision": args.precision, "parallelism": "single",
                    "l2": "working set > 126 MB L2 (no flush needed)"},
         "gups_A": N ** 3 * V / (t_a * 1e-3) / 1e9, "gups_AT": N ** 3 * V / (t_at * 1e-3) / 1e9,
         "ms_A": t_a, "ms_AT": t_at, "ms_rest_of_step": ms_step - t_a - t_at,
-        "loop": "device-resident CGLS, CUDA-graph replay per iteration",
+        "loop": loop,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": int(launches),
         "setup_s": t_setup, "plan_table_bytes": int(op.info.table_bytes),
         "plan": {"proj_chunk": int(op.info.proj_chunk), "bp_groups": int(op.info.bp_groups),
                  "bp_view_batches": int(op.info.bp_view_batches), "bp_closed_form": int(op.info.bp_closed_form)},
-        "e_last": run.rel(run.nb),
+        "e_last": e_last,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -450,7 +559,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
+    ap.add_argument("--solver", default=None, choices=sorted(SOLVER_METHOD),
+                    help="solver of the timed step (default: the config's, BASELINE.json: cgls, config 4 lsqr-jacobi)")
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
+                    help="operator / vector precision (f64: the reference-precision path, csrc/f64.cu)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--sharded", action="store_true", help="use the sharded (multi-GPU) driver even at N=1")

@@ -604,75 +604,98 @@ def _proj_update(dev, chain, e, p, alpha):
     return nb2, nb2
 
 
+class LsqrRun:
+    """LSQR state (solvers.py:361-459): the pre-loop (``__init__``: u = b - A x0, beta, 1 A^T,
+    alpha) and one loop iteration (``step``: 1 A + 1 A^T, the normalisations and the Givens
+    update).  ``lsqr`` drives it; the benchmark times ``step``."""
+
+    def __init__(self, op, b, cfg: SolverConfig):
+        self.op, self.b, self.cfg = op, b, cfg
+        self.dev = dev = _Dev(op)
+        self.chain = chain = _build_chain(op, cfg, dev)
+        self.t0 = time.perf_counter()
+        self.b_int = _as_internal_proj(op, b)
+        self.x = chain.z_of(_x0_internal(op, cfg, dev)).clone()
+        b_eff = chain.rhs(self.b_int)
+        self.nb0 = _norm(dev, self.b_int)
+        self.history = []
+        self.updates = 0
+        self.done = False
+        self.breakdown = False
+        self.u = u = dev.empty(chain.m_phys)
+        chain.apply(self.x, u)
+        beta = float(np.sqrt(dev.sub(b_eff, u, u, norm2=True)))
+        self.phibar = beta
+        if beta == 0.0:
+            self._record(0, 0.0)
+            self.done = self.breakdown = True
+            return
+        dev.div(u, beta)
+        self.v = v = dev.empty(chain.n_phys)
+        alpha = float(np.sqrt(chain.applyT(u, v, norm2=True)))
+        if alpha == 0.0:
+            self._record(0, self.rel(beta))
+            self.done = self.breakdown = True
+            return
+        dev.div(v, alpha)
+        self.w = v.clone()
+        self.alpha, self.rhobar = alpha, alpha
+        self.tmp_m = torch.empty_like(u)
+        self.tmp_n = torch.empty_like(v)
+
+    def rel(self, v):
+        return v / self.nb0 if self.nb0 > 0 else 0.0
+
+    def _record(self, i, e):
+        true_e = None
+        if _want_true(self.cfg, i):
+            true_e = _true_rel(self.op, self.chain, self.x, self.b_int, self.nb0, self.dev)
+        self.history.append(ConvergenceRecord(i, time.perf_counter() - self.t0, e, true_e))
+
+    def should_continue(self) -> bool:
+        return not self.done and self.updates < self.cfg.max_iterations + 1
+
+    def step(self) -> None:
+        """One bidiagonalisation step + Givens update + record (solvers.py:427-458)."""
+        dev, chain, u, v = self.dev, self.chain, self.u, self.v
+        alpha = self.alpha
+        chain.apply(v, self.tmp_m)
+        beta = float(np.sqrt(dev.axpby(1.0, self.tmp_m, -alpha, u, norm2=True)))  # u = A v - alpha u
+        if beta > 0.0:
+            dev.div(u, beta)
+            chain.applyT(u, self.tmp_n)
+            alpha = float(np.sqrt(dev.axpby(1.0, self.tmp_n, -beta, v, norm2=True)))  # v = A^T u - beta v
+            if alpha > 0.0:
+                dev.div(v, alpha)
+        rho = float(np.hypot(self.rhobar, beta))
+        c, s = self.rhobar / rho, beta / rho
+        theta = s * alpha
+        self.rhobar = -c * alpha
+        phi = c * self.phibar
+        self.phibar = s * self.phibar
+        self.alpha = alpha
+        dev.update2(self.x, self.w, v, phi / rho, True, -(theta / rho))  # x += (phi/rho) w ; w = v - (theta/rho) w
+        self._record(self.updates, self.rel(self.phibar))
+        self.updates += 1
+        err = self.cfg.rel_discrepancy_tol
+        if beta == 0.0 or alpha == 0.0:
+            self.done = self.breakdown = True
+        elif err > 0.0 and self.rel(self.phibar) <= err:
+            self.done = True
+
+    def report(self) -> SolverReport:
+        op = self.op
+        return SolverReport(_final_volume(op, self.chain.x_of(self.x), self.b.data), len(self.history) - 1,
+                            self.phibar, self.history, getattr(op, "workers", 1), self.breakdown)
+
+
 def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
     """LSQR (solvers.py:361-459): Golub-Kahan bidiagonalisation + Givens."""
     _check_inputs(op, b, cfg, "lsqr")
-    dev = _Dev(op)
-    chain = _build_chain(op, cfg, dev)
-    t0 = time.perf_counter()
-    b_int = _as_internal_proj(op, b)
-    x = chain.z_of(_x0_internal(op, cfg, dev)).clone()
-    b_eff = chain.rhs(b_int)
-    nb0 = _norm(dev, b_int)
-    history = []
-
-    def rel(v):
-        return v / nb0 if nb0 > 0 else 0.0
-
-    def record(i, e):
-        true_e = None
-        if _want_true(cfg, i):
-            true_e = _true_rel(op, chain, x, b_int, nb0, dev)
-        history.append(ConvergenceRecord(i, time.perf_counter() - t0, e, true_e))
-
-    def finish(i, phibar, breakdown):
-        return SolverReport(_final_volume(op, chain.x_of(x), b.data), i, phibar, history,
-                            getattr(op, "workers", 1), breakdown)
-
-    u = dev.empty(chain.m_phys)
-    chain.apply(x, u)
-    beta = float(np.sqrt(dev.sub(b_eff, u, u, norm2=True)))
-    if beta == 0.0:
-        record(0, 0.0)
-        return finish(0, 0.0, True)
-    dev.div(u, beta)
-    v = dev.empty(chain.n_phys)
-    alpha = float(np.sqrt(chain.applyT(u, v, norm2=True)))
-    if alpha == 0.0:
-        record(0, rel(beta))
-        return finish(0, beta, True)
-    dev.div(v, alpha)
-    w = v.clone()
-    phibar, rhobar = beta, alpha
-    tmp_m = torch.empty_like(u)
-    tmp_n = torch.empty_like(v)
-    err = cfg.rel_discrepancy_tol
-    updates = 0
-    breakdown = False
-    while updates < cfg.max_iterations + 1:
-        chain.apply(v, tmp_m)
-        beta = float(np.sqrt(dev.axpby(1.0, tmp_m, -alpha, u, norm2=True)))  # u = A v - alpha u
-        if beta > 0.0:
-            dev.div(u, beta)
-            chain.applyT(u, tmp_n)
-            alpha = float(np.sqrt(dev.axpby(1.0, tmp_n, -beta, v, norm2=True)))  # v = A^T u - beta v
-            if alpha > 0.0:
-                dev.div(v, alpha)
-        rho = float(np.hypot(rhobar, beta))
-        c, s = rhobar / rho, beta / rho
-        theta = s * alpha
-        rhobar = -c * alpha
-        phi = c * phibar
-        phibar = s * phibar
-        dev.update2(x, w, v, phi / rho, True, -(theta / rho))  # x += (phi/rho) w ; w = v - (theta/rho) w
-        record(updates, rel(phibar))
-        updates += 1
-        if beta == 0.0 or alpha == 0.0:
-            breakdown = True
-            break
-        if err > 0.0 and rel(phibar) <= err:
-            break
-    return finish(len(history) - 1, phibar, breakdown)
+    run = LsqrRun(op, b, cfg)
+    while run.should_continue():
+        run.step()
+    return run.report()
 
 
 def _inv_positive(t):
@@ -716,60 +739,85 @@ def psirt_step_scale(op, relaxation: float = 1.0) -> float:
     return 2.0 * relaxation / (_PSIRT_SPECTRAL_SAFETY * normal_spectral_radius(op))
 
 
+class ClassicalRun:
+    """SIRT / PSIRT state (solvers.py:505-569): the setup (``__init__``: row and column sums,
+    the PSIRT step from the spectral radius, r = b - A x0) and one iteration (``step``:
+    x += step A^T R^-1 r, optional clip, r = b - A x)."""
+
+    def __init__(self, op, b, cfg: SolverConfig, method: str):
+        self.op, self.b, self.cfg, self.method = op, b, cfg, method
+        self.dev = dev = _Dev(op)
+        self.t0 = time.perf_counter()
+        row = _as_internal_proj(op, _call_sums(op, "row_sums"))
+        col = _as_internal_volume(op, _call_sums(op, "col_sums"))
+        if not bool((row > 0).any()) or not bool((col > 0).any()):
+            raise DegenerateOperatorError("operator never intersects the volume")
+        self.inv_row = _inv_positive(row)
+        del row
+        if method == "sirt":
+            self.step_vec = (cfg.relaxation * _inv_positive(col)).to(dev.dtype)
+            self.step_size = None
+        else:
+            self.step_vec = None
+            self.step_size = 2.0 * cfg.relaxation / (_PSIRT_SPECTRAL_SAFETY * _spectral(op, dev, self.inv_row, 10))
+        del col
+        self.b_int = _as_internal_proj(op, b)
+        self.x = _x0_internal(op, cfg, dev)
+        self.nb0 = _norm(dev, self.b_int)
+        self.lo, self.hi = cfg.box_bounds if cfg.box_bounds is not None else (None, None)
+        self.history = []
+        self.chain = _Chain(op, dev)
+        self.resid = dev.empty(op.m)
+        self.weighted = torch.empty_like(self.resid)
+        self.upd = dev.empty(dev.vol_elems)
+        self.chain.apply(self.x, self.resid)
+        self.e = self.rel(float(np.sqrt(dev.sub(self.b_int, self.resid, self.resid, norm2=True))))
+        self._record(0)
+        self.i = 0
+
+    def rel(self, v):
+        return v / self.nb0 if self.nb0 > 0 else 0.0
+
+    def _record(self, i):
+        e = self.e
+        self.history.append(ConvergenceRecord(i, time.perf_counter() - self.t0, e,
+                                              e if _want_true(self.cfg, i) else None))
+
+    def should_continue(self) -> bool:
+        err = self.cfg.rel_discrepancy_tol
+        return (err == 0.0 or self.e > err) and self.i < self.cfg.max_iterations
+
+    def step(self) -> None:
+        dev, chain = self.dev, self.chain
+        dev.mul(self.resid, self.inv_row, self.weighted)
+        chain.applyT(self.weighted, self.upd)
+        if self.step_vec is not None:
+            dev.mul(self.upd, self.step_vec, self.upd)
+            dev.axpby(1.0, self.upd, 1.0, self.x)
+        else:
+            dev.axpby(self.step_size, self.upd, 1.0, self.x)
+        if self.lo is not None:
+            dev.clip(self.x, self.lo, self.hi)
+        chain.apply(self.x, self.resid)
+        self.e = self.rel(float(np.sqrt(dev.sub(self.b_int, self.resid, self.resid, norm2=True))))
+        self.i += 1
+        self._record(self.i)
+
+    def report(self) -> SolverReport:
+        op = self.op
+        return SolverReport(_final_volume(op, self.x, self.b.data), self.i, self.e * self.nb0, self.history,
+                            getattr(op, "workers", 1), False)
+
+
 def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solvers.py:505-569
     _check_inputs(op, b, cfg, method)
-    dev = _Dev(op)
-    t0 = time.perf_counter()
-    row = _as_internal_proj(op, _call_sums(op, "row_sums"))
-    col = _as_internal_volume(op, _call_sums(op, "col_sums"))
-    if not bool((row > 0).any()) or not bool((col > 0).any()):
-        raise DegenerateOperatorError("operator never intersects the volume")
-    inv_row = _inv_positive(row)
-    if method == "sirt":
-        step_vec = (cfg.relaxation * _inv_positive(col)).to(dev.dtype)
-        step = None
-    else:
-        step_vec = None
-        step = 2.0 * cfg.relaxation / (_PSIRT_SPECTRAL_SAFETY * _spectral(op, dev, inv_row, 10))
-    del col
-    b_int = _as_internal_proj(op, b)
-    x = _x0_internal(op, cfg, dev)
-    nb0 = _norm(dev, b_int)
-    lo, hi = cfg.box_bounds if cfg.box_bounds is not None else (None, None)
-    history = []
-    chain = _Chain(op, dev)
-
-    def rel(v):
-        return v / nb0 if nb0 > 0 else 0.0
-
-    def record(i, e):
-        history.append(ConvergenceRecord(i, time.perf_counter() - t0, e, e if _want_true(cfg, i) else None))
-
-    resid = dev.empty(op.m)
-    weighted = torch.empty_like(resid)
-    upd = dev.empty(dev.vol_elems)
-    chain.apply(x, resid)
-    e = rel(float(np.sqrt(dev.sub(b_int, resid, resid, norm2=True))))
-    record(0, e)
+    run = ClassicalRun(op, b, cfg, method)
     err = cfg.rel_discrepancy_tol
-    i = 0
-    while (err == 0.0 or e > err) and i < cfg.max_iterations:
-        dev.mul(resid, inv_row, weighted)
-        chain.applyT(weighted, upd)
-        if step_vec is not None:
-            dev.mul(upd, step_vec, upd)
-            dev.axpby(1.0, upd, 1.0, x)
-        else:
-            dev.axpby(step, upd, 1.0, x)
-        if lo is not None:
-            dev.clip(x, lo, hi)
-        chain.apply(x, resid)
-        e = rel(float(np.sqrt(dev.sub(b_int, resid, resid, norm2=True))))
-        i += 1
-        record(i, e)
-        if err > 0.0 and e <= err:
+    while run.should_continue():
+        run.step()
+        if err > 0.0 and run.e <= err:
             break
-    return SolverReport(_final_volume(op, x, b.data), i, e * nb0, history, getattr(op, "workers", 1), False)
+    return run.report()
 
 
 def sirt(op, b, cfg: SolverConfig) -> SolverReport:
