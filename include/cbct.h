@@ -91,7 +91,8 @@ typedef struct cbct_plan_info {
     int32_t proj_chunk;        /* cells per chunk of the prefix-sum projector (0: another projector) */
     int32_t bp_groups;         /* boundary groups per warp of the boundary-form backprojector */
     int32_t bp_view_batches;   /* launches of one mode-1 backprojection (view batches) */
-    int32_t reserved;
+    int32_t bp_sided_gs;       /* 0: mode-1 A^T runs k_bp_boundary; g > 0: k_bp_sided with g below + g above
+                                  boundary groups per warp */
 } cbct_plan_info;
 
 /* ---- plan lifecycle ------------------------------------------------------ */

@@ -45,7 +45,7 @@ class PlanInfo(ctypes.Structure):
         ("max_cell_entries", c_i64), ("table_bytes", c_i64),
         ("proj_blocks", c_i32), ("bp_blocks", c_i32),
         ("bp_scratch_floats", c_i64), ("bp_fast_path", c_i32), ("bp_closed_form", c_i32),
-        ("proj_chunk", c_i32), ("bp_groups", c_i32), ("bp_view_batches", c_i32), ("reserved", c_i32),
+        ("proj_chunk", c_i32), ("bp_groups", c_i32), ("bp_view_batches", c_i32), ("bp_sided_gs", c_i32),
     ]
 
 

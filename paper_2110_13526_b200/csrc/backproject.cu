@@ -428,6 +428,149 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sided variant of the closed-form boundary kernel.  The boundary form needs, per
+// boundary, which end of the crossing bounds a ray's height (t_b above the mid-plane,
+// t_a below) and whether the straddle fraction is f_t or 1 - f_t.  k_bp_boundary blends
+// both per lane with sign registers; at 64 registers and six groups the compiler
+// rematerialises them every entry (~5 of ~23 instructions per boundary).  Here the
+// boundaries are grouped so that every group lies on one side: above groups start at k0
+// (the first boundary with z >= 0) and run up, below groups end at k0 and run down, and
+// each warp runs GS below groups and GS above groups with the side known at compile time.
+// The top below group's last lane sits on z_k0; the plan only selects this kernel when
+// that boundary is exactly z = 0 (or one side is empty), where the below formula with
+// z = -0 (1/z = -inf) yields the above formula's value: no ray straddles the plane z = 0
+// (rays through the source height are the separate flat row).
+template <int GS, bool FLAT>
+__global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict__ cell_off,
+                                                    const CellEntry* __restrict__ cell_ent,
+                                                    const ColumnHeader* __restrict__ cols,
+                                                    const float* __restrict__ pref, const float* __restrict__ flatw,
+                                                    float* __restrict__ vol, const float* __restrict__ col_scale,
+                                                    double* __restrict__ partials, int nv, int nz, int zs,
+                                                    double lo2, double p2, double det00z, double pv, int nx,
+                                                    int row0, int row1, int pad_lo, int pad_hi,
+                                                    const int32_t* __restrict__ boff, int nb, int vb, int accum,
+                                                    int k0, int zero_at_k0) {
+    constexpr int G = 2 * GS;  // groups [0, GS): below, [GS, 2 GS): above
+    __shared__ float4 s_t0[kChunk], s_t1[kChunk];
+    __shared__ int s_vu[kChunk], s_fs[kChunk];
+    const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
+    if (cell < 0) {
+        if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
+        return;
+    }
+    int64_t off = cell_off[cell];
+    int ne = (int)(cell_off[cell + 1] - off);
+    if (boff) {
+        const int32_t* bo = boff + cell * (nb + 1) + vb;
+        off += bo[0];
+        ne = bo[1] - bo[0];
+    }
+    const int nvq = nv + 2 + pad_lo + pad_hi;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float z[G], zlo[G], acc[G], iz[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int gi = warp * GS + (g < GS ? g : g - GS);
+        const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;  // boundary index
+        const int kc = min(max(kb, 0), nz);  // lanes outside the volume reuse an end (results unused)
+        const double zd = lo2 + (double)kc * p2;
+        z[g] = (float)zd;
+        zlo[g] = (float)(zd - (double)z[g]);
+        iz[g] = (float)(1.0 / zd);
+        if (g < GS && kc == k0 && zero_at_k0) {  // z_k0 = 0 seen from below: -0 and 1/z = -inf
+            z[g] = -0.0f;
+            zlo[g] = 0.0f;
+            iz[g] = -INFINITY;
+        }
+        acc[g] = 0.0f;
+    }
+    const double c0d = -det00z / pv;
+    const double c0i = floor(c0d + 0.5);
+    const float c0f = (float)(c0d - c0i);
+    const int magic = 0x4B400000 - (int)c0i - 1;
+    const float fpv = (float)pv;
+
+    for (int base = 0; base < ne; base += kChunk) {
+        const int nch = min(kChunk, ne - base);
+        __syncthreads();
+        for (int k = threadIdx.x; k < nch; k += blockDim.x) {
+            const CellEntry ce = cell_ent[off + base + k];
+            const ColumnHeader& h = cols[ce.vu];
+            const float ta = ce.tau_a, tb = ce.tau_b, tr = h.t_ref;
+            const float dt = tb - ta;
+            const float taa = ta + tr, tba = tb + tr;
+            const double iad = 1.0 / (((double)ta + (double)tr) * pv);
+            const float ia = (float)iad, ia_lo = (float)(iad - (double)ia);
+            const float ib = (float)(1.0 / (((double)tb + (double)tr) * pv));
+            // {1/(t_a pv), 1/(t_b pv), kI = pv t_a t_b / dt, dt}, {eps = dt / t_a, 1/(t_a pv) (lo), 1 - eps, flat}
+            s_t0[k] = make_float4(ia, ib, dt > 0.0f ? fpv * taa * tba / dt : 0.0f, dt);
+            s_t1[k] = make_float4(dt / taa, ia_lo, 1.0f - dt / taa, FLAT ? flatw[ce.vu] : 0.0f);
+            s_vu[k] = ce.vu;
+            s_fs[k] = FLAT ? cols[ce.vu].flat_slab : 0;
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int k = 0; k < nch; ++k) {
+            const float4 t0 = s_t0[k], t1 = s_t1[k];
+            const float2* pyc = reinterpret_cast<const float2*>(pref) + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq +
+                                pad_lo - (uint32_t)magic;
+            asm("mov.b64 %0, %0;" : "+l"(pyc));
+            float P0[G], P1[G];
+            uint32_t bg[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                // rays entirely below z: rows under W(t_b) above the mid-plane, W(t_a) below
+                const float W = fmaf(z[g], g < GS ? t0.x : t0.y, c0f);
+                bg[g] = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));
+                const float2 py = __ldg(pyc + bg[g]);
+                P0[g] = py.x;
+                P1[g] = py.y;
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                // straddle fraction (closed form, k_bp_boundary): s in 1/t, f_t = s (1 - eps + eps s)
+                const float R = __int_as_float((int)bg[g]) - 12582911.0f;
+                const float tail = fmaf(zlo[g], t0.x, fmaf(z[g], t1.y, c0f));
+                const float sv = __saturatef((fmaf(z[g], t0.x, -R) + tail) * (iz[g] * t0.z));
+                const float h = fmaf(t1.x, sv, t1.z);
+                const float f = g < GS ? fmaf(-sv, h, 1.0f) : sv * h;  // below: 1 - f_t ; above: f_t
+                const float Gv = fmaf(f, P1[g], P0[g]);
+                const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
+                acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
+                if (FLAT) {
+                    const int gi = warp * GS + (g < GS ? g : g - GS);
+                    const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;
+                    acc[g] += (kb == s_fs[k]) ? t0.w * t1.w : 0.0f;
+                }
+            }
+        }
+    }
+
+    const int64_t lcell = cell - (int64_t)row0 * nx;
+    float* out = vol + lcell * zs;
+    double sq = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int gi = warp * GS + (g < GS ? g : g - GS);
+        const int kv = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;  // voxel [z_kv, z_kv+1)
+        const bool mine = lane < 31 && kv >= 0 && kv < nz && (g < GS ? kv < k0 : kv >= k0);
+        if (mine) {
+            float val = acc[g];
+            if (col_scale) val *= col_scale[lcell * zs + CBCT_ZPAD + kv];
+            if (accum) val += out[CBCT_ZPAD + kv];
+            out[CBCT_ZPAD + kv] = val;
+            sq += (double)val * (double)val;
+        }
+    }
+    for (int k = threadIdx.x; k < zs - nz; k += blockDim.x) out[k < CBCT_ZPAD ? k : nz + k] = 0.0f;
+    if (partials) {
+        const double tot = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+    }
+}
+
 }  // namespace
 
 extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, float* vol, int64_t row0, int64_t row1,
@@ -479,8 +622,25 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         // norm partials
         const int nb = p->bp_vbatch;
         const int32_t* boff = nb > 1 ? p->d_cell_boff : nullptr;
+        const bool sided = !table && p->bps_ok;
+#define LAUNCH_S(GS, FL)                                                                                       \
+        k_bp_sided<GS, FL><<<grid, p->bps_threads, 0, s>>>(                                                   \
+            p->d_cell_off, p->d_cell_ent, p->d_cols, pyb, flatw, vol, col_scale, part, (int)p->nv, (int)p->nz, \
+            (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx, (int)row0, (int)row1,             \
+            p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0, p->bps_k0, p->bps_zero)
         for (int vb = 0; vb < nb; ++vb) {
             double* part = vb == nb - 1 ? partials : nullptr;
+            if (sided) {
+                switch (p->bps_gs * 2 + (fl ? 1 : 0)) {
+                    case 2: LAUNCH_S(1, false); break;
+                    case 3: LAUNCH_S(1, true); break;
+                    case 4: LAUNCH_S(2, false); break;
+                    case 5: LAUNCH_S(2, true); break;
+                    case 6: LAUNCH_S(3, false); break;
+                    default: LAUNCH_S(3, true); break;
+                }
+                continue;
+            }
             switch (p->bpg_groups * 2 + (fl ? 1 : 0)) {
                 case 2: LAUNCH_G(1, false); break;
                 case 3: LAUNCH_G(1, true); break;
@@ -497,6 +657,7 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
             }
         }
 #undef LAUNCH_G
+#undef LAUNCH_S
         CBCT_CHECK(cudaGetLastError());
         cbct_count_launch(1 + nb);
         return 0;

@@ -75,6 +75,10 @@ struct cbct_plan {
     int proj_q, proj_q_c, proj_q_zr;            // column prefix-sum projector (chunk of C cells, zero row)
     int bp_threads, bp_zpt;
     int bpg_threads, bpg_groups;  // boundary-form backprojector shape
+    // sided boundary kernel (k_bp_sided): GS below + GS above groups per warp, anchored at the
+    // first boundary k0 with z >= 0; usable when z_k0 == 0 exactly or one side is empty
+    bool bps_ok = false;
+    int bps_gs = 0, bps_threads = 0, bps_k0 = 0, bps_zero = 0;
     bool bp_boundary_ok;          // at most one ray straddles any voxel boundary per crossing
     int32_t bp_pad_lo, bp_pad_hi; // rows of the ray-prefix table below 0 / above nv (no index clamping)
     bool bp_closed_ok;            // eps = max dtau / min t small enough for the closed-form straddle

@@ -549,6 +549,35 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         p->bpg_groups = best_g;
         p->bpg_threads = (int)(((groups + best_g - 1) / best_g) * 32);
     }
+    {
+        // sided groups (backproject.cu k_bp_sided): below groups end at k0, above groups start there
+        int64_t k0 = g->nz + 1;
+        for (int64_t k = 0; k <= g->nz; ++k)
+            if (g->lo[2] + (double)k * g->pitch[2] >= 0.0) { k0 = k; break; }
+        const bool both = k0 > 0 && k0 <= g->nz;
+        const bool zero = both && g->lo[2] + (double)k0 * g->pitch[2] == 0.0;
+        const int64_t nb = (std::min<int64_t>(k0, g->nz) + 30) / 31;
+        const int64_t na = (std::max<int64_t>(g->nz - k0, 0) + 30) / 31;
+        // GS in {2, 3} with the least wasted group slots, ties to GS = 2; the sided kernel is used
+        // when at most 10% of its slots are wasted (measured A^T: config 3 GS=3 114 ms vs 128 ms
+        // for k_bp_boundary; config 5 GS=2 1469 vs 1684 ms; config 2 with 2 of 12 slots wasted
+        // 15.1 vs 14.1 ms, so it keeps k_bp_boundary)
+        int best = 0;
+        int64_t best_waste = INT64_MAX, best_slots = 1;
+        for (int gs : {3, 2}) {
+            const int64_t warps = (std::max(nb, na) + gs - 1) / gs;
+            if (warps > 32) continue;
+            const int64_t waste = warps * gs * 2 - nb - na;
+            if (waste <= best_waste) { best_waste = waste; best = gs; best_slots = warps * gs * 2; }
+        }
+        bool use = best > 0 && 10 * best_waste <= best_slots;
+        if (const char* e = getenv("CBCT_BP_GS")) { best = atoi(e); use = best > 0; }
+        p->bps_ok = (!both || zero) && use && getenv("CBCT_BP_SIDED_OFF") == nullptr;
+        p->bps_gs = best;
+        p->bps_threads = best > 0 ? (int)((std::max(nb, na) + best - 1) / best * 32) : 0;
+        p->bps_k0 = (int)k0;
+        p->bps_zero = zero ? 1 : 0;
+    }
     p->table_bytes = total;
     cudaFree(d_counts); cudaFree(d_cellkey);  // d_srcs/d_det00/d_ustep belong to the plan
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
@@ -584,6 +613,7 @@ extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {
     info->proj_chunk = p->proj_q ? p->proj_q_c : 0;
     info->bp_groups = p->bpg_groups;
     info->bp_view_batches = p->bp_vbatch;
-    info->reserved = 0;
+    const bool closed = p->bp_boundary_ok && p->bp_closed_ok && !getenv("CBCT_BP_TABLE");
+    info->bp_sided_gs = (closed && p->bps_ok) ? p->bps_gs : 0;
     return 0;
 }
