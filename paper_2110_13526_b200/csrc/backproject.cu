@@ -441,8 +441,8 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
 // that boundary is exactly z = 0 (or one side is empty), where the below formula with
 // z = -0 (1/z = -inf) yields the above formula's value: no ray straddles the plane z = 0
 // (rays through the source height are the separate flat row).
-template <int GS, bool FLAT>
-__global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict__ cell_off,
+template <int GS, bool FLAT, int MAXR>
+__global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_off,
                                                     const CellEntry* __restrict__ cell_ent,
                                                     const ColumnHeader* __restrict__ cols,
                                                     const float* __restrict__ pref, const float* __restrict__ flatw,
@@ -454,7 +454,9 @@ __global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict_
                                                     int k0, int zero_at_k0) {
     constexpr int G = 2 * GS;  // groups [0, GS): below, [GS, 2 GS): above
     __shared__ float4 s_t0[kChunk], s_t1[kChunk];
-    __shared__ int s_vu[kChunk], s_fs[kChunk];
+    __shared__ float2 s_t2[kChunk];
+    __shared__ long long s_base[kChunk];
+    __shared__ int s_fs[FLAT ? kChunk : 1];
     const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
     if (cell < 0) {
         if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
@@ -469,28 +471,28 @@ __global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict_
     }
     const int nvq = nv + 2 + pad_lo + pad_hi;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float z[G], zlo[G], acc[G], iz[G];
+    // Boundary heights are z = z_off + zp p2 with zp = k - k0 an exact small integer in fp32, so
+    // z / (t pv) = zp (p2 / (t pv)) + z_off / (t pv): the per-crossing slopes p2/(t pv) carry the
+    // precision (two fp32 words for the t_a slope) and z needs no second word.
+    const int kk0 = min(k0, nz);
+    const double zoff = lo2 + (double)kk0 * p2;  // z at k0 (0 when both sides are present)
+    float zp[G], acc[G], iz[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int gi = warp * GS + (g < GS ? g : g - GS);
         const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;  // boundary index
         const int kc = min(max(kb, 0), nz);  // lanes outside the volume reuse an end (results unused)
-        const double zd = lo2 + (double)kc * p2;
-        z[g] = (float)zd;
-        zlo[g] = (float)(zd - (double)z[g]);
-        iz[g] = (float)(1.0 / zd);
+        zp[g] = (float)(kc - kk0);
+        iz[g] = (float)(1.0 / (zoff + (double)(kc - kk0) * p2));
         if (g < GS && kc == k0 && zero_at_k0) {  // z_k0 = 0 seen from below: -0 and 1/z = -inf
-            z[g] = -0.0f;
-            zlo[g] = 0.0f;
+            zp[g] = -0.0f;
             iz[g] = -INFINITY;
         }
         acc[g] = 0.0f;
     }
     const double c0d = -det00z / pv;
-    const double c0i = floor(c0d + 0.5);
-    const float c0f = (float)(c0d - c0i);
-    const int magic = 0x4B400000 - (int)c0i - 1;
-    const float fpv = (float)pv;
+    // side of the row lookup when only one side exists (with both, z_off = 0 and both agree)
+    const bool look_b = k0 == 0;
 
     for (int base = 0; base < ne; base += kChunk) {
         const int nch = min(kChunk, ne - base);
@@ -502,27 +504,35 @@ __global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict_
             const float dt = tb - ta;
             const float taa = ta + tr, tba = tb + tr;
             const double iad = 1.0 / (((double)ta + (double)tr) * pv);
-            const float ia = (float)iad, ia_lo = (float)(iad - (double)ia);
-            const float ib = (float)(1.0 / (((double)tb + (double)tr) * pv));
-            // {1/(t_a pv), 1/(t_b pv), kI = pv t_a t_b / dt, dt}, {eps = dt / t_a, 1/(t_a pv) (lo), 1 - eps, flat}
-            s_t0[k] = make_float4(ia, ib, dt > 0.0f ? fpv * taa * tba / dt : 0.0f, dt);
-            s_t1[k] = make_float4(dt / taa, ia_lo, 1.0f - dt / taa, FLAT ? flatw[ce.vu] : 0.0f);
-            s_vu[k] = ce.vu;
-            s_fs[k] = FLAT ? cols[ce.vu].flat_slab : 0;
+            const double ibd = 1.0 / (((double)tb + (double)tr) * pv);
+            const double sad = p2 * iad;
+            const float sa = (float)sad, sa_lo = (float)(sad - (double)sa);
+            // row coordinates at z_off: W = zp * slope + B; B's integer part goes into the table base
+            const double Ba = zoff * iad + c0d;
+            const double Bl = look_b ? zoff * ibd + c0d : Ba;
+            const double Bi = floor(Bl + 0.5);
+            const int magic = 0x4B400000 - (int)Bi - 1;  // floor(W) + Bi + 1 via the 1.5*2^23 trick
+            // {p2/(t_a pv), p2/(t_b pv), kI = pv t_a t_b / dt, dt}, {eps = dt / t_a, p2/(t_a pv) lo, 1 - eps, flat},
+            // {lookup B fraction, W_a offset relative to the lookup's integer}
+            s_t0[k] = make_float4(sa, (float)(p2 * ibd), dt > 0.0f ? (float)pv * taa * tba / dt : 0.0f, dt);
+            s_t1[k] = make_float4(dt / taa, sa_lo, 1.0f - dt / taa, FLAT ? flatw[ce.vu] : 0.0f);
+            s_t2[k] = make_float2((float)(Bl - Bi), (float)(Ba - Bi));
+            s_base[k] = (long long)ce.vu * nvq + pad_lo - (long long)magic;
+            if (FLAT) s_fs[k] = cols[ce.vu].flat_slab;
         }
         __syncthreads();
 #pragma unroll 2
         for (int k = 0; k < nch; ++k) {
             const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float2* pyc = reinterpret_cast<const float2*>(pref) + (size_t)(uint32_t)s_vu[k] * (uint32_t)nvq +
-                                pad_lo - (uint32_t)magic;
+            const float2 t2 = s_t2[k];
+            const float2* pyc = reinterpret_cast<const float2*>(pref) + s_base[k];
             asm("mov.b64 %0, %0;" : "+l"(pyc));
             float P0[G], P1[G];
             uint32_t bg[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 // rays entirely below z: rows under W(t_b) above the mid-plane, W(t_a) below
-                const float W = fmaf(z[g], g < GS ? t0.x : t0.y, c0f);
+                const float W = fmaf(zp[g], g < GS ? t0.x : t0.y, t2.x);
                 bg[g] = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));
                 const float2 py = __ldg(pyc + bg[g]);
                 P0[g] = py.x;
@@ -530,10 +540,11 @@ __global__ void __launch_bounds__(1024, 1) k_bp_sided(const int64_t* __restrict_
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                // straddle fraction (closed form, k_bp_boundary): s in 1/t, f_t = s (1 - eps + eps s)
+                // straddle fraction (closed form, k_bp_boundary): s = (W_a - R) kI / z in 1/t,
+                // f_t = s (1 - eps + eps s); W_a - R = zp sa + (B_a - Bi) - R with every rounding on O(1)
                 const float R = __int_as_float((int)bg[g]) - 12582911.0f;
-                const float tail = fmaf(zlo[g], t0.x, fmaf(z[g], t1.y, c0f));
-                const float sv = __saturatef((fmaf(z[g], t0.x, -R) + tail) * (iz[g] * t0.z));
+                const float u = fmaf(zp[g], t1.y, fmaf(zp[g], t0.x, t2.y - R));
+                const float sv = __saturatef(u * (iz[g] * t0.z));
                 const float h = fmaf(t1.x, sv, t1.z);
                 const float f = g < GS ? fmaf(-sv, h, 1.0f) : sv * h;  // below: 1 - f_t ; above: f_t
                 const float Gv = fmaf(f, P1[g], P0[g]);
@@ -623,11 +634,21 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         const int nb = p->bp_vbatch;
         const int32_t* boff = nb > 1 ? p->d_cell_boff : nullptr;
         const bool sided = !table && p->bps_ok;
-#define LAUNCH_S(GS, FL)                                                                                       \
-        k_bp_sided<GS, FL><<<grid, p->bps_threads, 0, s>>>(                                                   \
+        // register cap of the sided kernel: 56 for GS = 3 (11 CTAs of 96 threads instead of 10; config 3
+        // A^T 107.8 -> 105.7 ms), 64 for GS = 2 (config 5: 56 regs spill, 1379 vs 1418 ms)
+        static const int regs_env = getenv("CBCT_BP_REGS") ? atoi(getenv("CBCT_BP_REGS")) : 0;
+        const int sided_regs = regs_env ? regs_env : (p->bps_gs == 3 ? 56 : 64);
+#define LAUNCH_S1(GS, FL, MR)                                                                                  \
+        k_bp_sided<GS, FL, MR><<<grid, p->bps_threads, 0, s>>>(                                               \
             p->d_cell_off, p->d_cell_ent, p->d_cols, pyb, flatw, vol, col_scale, part, (int)p->nv, (int)p->nz, \
             (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx, (int)row0, (int)row1,             \
             p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0, p->bps_k0, p->bps_zero)
+#define LAUNCH_S(GS, FL)                                                                                       \
+        do {                                                                                                   \
+            if (sided_regs == 48) LAUNCH_S1(GS, FL, 48);                                                       \
+            else if (sided_regs == 56) LAUNCH_S1(GS, FL, 56);                                                  \
+            else LAUNCH_S1(GS, FL, 64);                                                                        \
+        } while (0)
         for (int vb = 0; vb < nb; ++vb) {
             double* part = vb == nb - 1 ? partials : nullptr;
             if (sided) {
@@ -658,6 +679,7 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         }
 #undef LAUNCH_G
 #undef LAUNCH_S
+#undef LAUNCH_S1
         CBCT_CHECK(cudaGetLastError());
         cbct_count_launch(1 + nb);
         return 0;
