@@ -442,19 +442,24 @@ def run_ours(args, cfg, rank, world, local_rank):
 
 
 def run_sharded(args, cfg, rank, world, local_rank):
-    """N > 1: one CGLS solve sharded over the ranks (views for A, cell rows for A^T), NCCL all_gathers
-    of d and e per iteration (paper_2110_13526_b200/distributed.py).  Strong scaling: total work fixed."""
+    """N > 1: one solve (CGLS, LSQR+Jacobi or PSIRT) sharded over the ranks (views for A, cell rows for
+    A^T), NCCL all_gathers of the volume and projection vectors before A and A^T
+    (paper_2110_13526_b200/distributed.py).  Strong scaling: total work fixed."""
     import torch
     import torch.distributed as dist
 
     import paper_2110_13526_b200 as P
     from paper_2110_13526_b200 import _lib
-    from paper_2110_13526_b200.distributed import CudaVectors, DistCglsRun, ShardedOperator, TorchComm
+    from paper_2110_13526_b200.distributed import (CudaVectors, DistCglsRun, DistClassicalRun, DistLsqrRun,
+                                                   ShardedOperator, TorchComm)
     from paper_2110_13526_b200.solvers import SolverConfig
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    N, V, nu, nv, solver, K = CONFIGS[cfg]
+    N, V, nu, nv, _, K = CONFIGS[cfg]
+    solver = args.solver or CONFIGS[cfg][4]
+    sname = SOLVER_NAME[solver]
+    method, kw = SOLVER_METHOD[solver]
     vg, tr = geometry(cfg)
     comm = TorchComm()
     sop = ShardedOperator(vg, tr, comm, device=dev)
@@ -470,21 +475,44 @@ def run_sharded(args, cfg, rank, world, local_rank):
     del b_full, truth
     vec = CudaVectors(op)
     steps, warmup = args.steps, args.warmup
-    run = DistCglsRun(sop, vec, b_local, SolverConfig(method="cgls", max_iterations=steps + warmup + 1), record=False)
+
+    def new_run(bl, iters, record=False):
+        scfg = SolverConfig(method=method, max_iterations=iters, **kw)
+        if method == "cgls":
+            return DistCglsRun(sop, vec, bl, scfg, record=record)
+        if method == "lsqr":
+            return DistLsqrRun(sop, vec, bl, scfg, record=record)
+        return DistClassicalRun(sop, vec, bl, scfg, method, record=record)
+
+    run = new_run(b_local, steps + warmup + 1)
     stream = torch.cuda.current_stream(dev)
-    # device-resident sharded loop: norm partials all-gathered and summed on the GPU, no host
-    # round trip inside the K iterations (distributed.DistCglsRun.run_device)
-    run.run_device(warmup)
-    dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = _lib.lib().cbct_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        start.record(stream)
-        run.run_device(steps)
-        end.record(stream)
+    if method == "cgls":
+        # device-resident sharded loop: norm partials all-gathered and summed on the GPU, no host
+        # round trip inside the K iterations (distributed.DistCglsRun.run_device)
+        run.run_device(warmup)
+        dist.barrier()
         torch.cuda.synchronize()
-    assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
+        launches0 = _lib.lib().cbct_launch_count()
+        with ClockSampler(local_rank) as clk:
+            start.record(stream)
+            run.run_device(steps)
+            end.record(stream)
+            torch.cuda.synchronize()
+        assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
+    else:
+        # host-driven sharded LSQR / PSIRT: rank-ordered fp64 scalar sums between the kernels
+        for _ in range(warmup):
+            run.step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = _lib.lib().cbct_launch_count()
+        with ClockSampler(local_rank) as clk:
+            start.record(stream)
+            for _ in range(steps):
+                run.step()
+            end.record(stream)
+            torch.cuda.synchronize()
     launches = _lib.lib().cbct_launch_count() - launches0
     t = torch.tensor([start.elapsed_time(end)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -501,8 +529,11 @@ def run_sharded(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         return s.elapsed_time(e) / reps
 
-    t_a = kernel_ms(lambda: sop.project_local(sop._d_full, run.p))
-    t_at = kernel_ms(lambda: sop.backproject_local(sop._e_full, run.r))
+    p_tmp = torch.zeros(sop.m_loc, device=dev)
+    r_tmp = torch.zeros(sop.n_loc, device=dev)
+    t_a = kernel_ms(lambda: sop.project_local(sop._d_full, p_tmp))
+    t_at = kernel_ms(lambda: sop.backproject_local(sop._e_full, r_tmp))
+    del p_tmp, r_tmp, run
     tk = torch.tensor([t_a, t_at], device=dev)
     dist.all_reduce(tk, op=dist.ReduceOp.MAX)
     t_a, t_at = (float(v) for v in tk.tolist())
@@ -513,9 +544,13 @@ def run_sharded(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     bl = b_host.to(dev, non_blocking=True)
-    r2 = DistCglsRun(sop, vec, bl, SolverConfig(method="cgls", max_iterations=e2e_k), record=False)
-    while r2.should_continue():
-        r2.run_device(e2e_k - r2.i)
+    r2 = new_run(bl, e2e_k)
+    if method == "cgls":
+        while r2.should_continue():
+            r2.run_device(e2e_k - r2.i)
+    else:
+        while r2.should_continue():
+            r2.step()
     _, x_loc = r2.finish()
     x_full = sop.gather_volume(x_loc)
     x_host = x_full[: op.vol_elems].cpu() if rank == 0 else None
@@ -532,10 +567,11 @@ def run_sharded(args, cfg, rank, world, local_rank):
     nnz_dom = nnz / world if dom == "A^T" else nnz_a
     achieved = SLOTS_PER_NNZ * nnz_dom / (t_dom * 1e-3)
     line = {
-        "metric": "CGLS iterations/sec", "value": 1e3 / ms_step, "unit": "it/s", "n_gpus": world, "steps": steps,
+        "metric": f"{sname} iterations/sec", "value": 1e3 / ms_step, "unit": "it/s", "n_gpus": world, "steps": steps,
         "warmup": warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, {sname} step",
+                   "solver": solver,
                    "parallelism": f"A by view x{world}, A^T by cell rows x{world}, " +
                                   ("fused d/e updates with NVLink peer stores" if args.p2p else "NCCL all_gather d/e"),
                    "l2": "working set > 126 MB L2 (no flush needed)"},
