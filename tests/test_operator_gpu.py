@@ -314,3 +314,36 @@ def test_row_and_col_sums_are_the_operator_on_ones():
     np.testing.assert_array_equal(rows, op.project(_vol(op, np.ones(op.n))).data)
     assert np.all(rows >= 0)
     np.testing.assert_array_equal(op.col_sums().data, op.backproject(_stack(op, np.ones(op.m))).data)
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_ray_segments_sum_to_chord(precision):
+    """test_operator.py:61-88: every ray's segment lengths sum to its clipped chord, over > 100
+    rays of three views (reference bar 1e-9 on the fp64 path; 1e-5 for fp32 lengths)."""
+    from paper_2110_13526_b200.geometry import detector_pixel_center, source_position
+    from paper_2110_13526_b200.operator import CbctOperator
+
+    d = load_golden("small_instance")
+    vg, tr = geom_from_golden(d)
+    op = CbctOperator(vg, tr, workers=3, precision=precision)
+    lo = np.asarray(vg.corner(), dtype=np.float64)
+    hi = lo + np.asarray(vg.extent)
+    checked = 0
+    for view in (0, 3, 5):
+        for u in range(8):
+            for v in range(8):
+                idx, lengths = op.ray_segments(view, u, v)
+                src = source_position(tr, view)
+                dvec = detector_pixel_center(tr, view, u, v) - src
+                tmin, tmax = 0.0, 1.0
+                for a in range(3):
+                    t1, t2 = (lo[a] - src[a]) / dvec[a], (hi[a] - src[a]) / dvec[a]
+                    tmin, tmax = max(tmin, min(t1, t2)), min(tmax, max(t1, t2))
+                if tmax <= tmin:
+                    assert lengths.size == 0
+                    continue
+                chord = (tmax - tmin) * np.linalg.norm(dvec)
+                assert lengths.sum() == pytest.approx(chord, rel=1e-9 if precision == "f64" else 1e-5)
+                assert np.all(lengths > 0)
+                checked += 1
+    assert checked > 100
