@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
                 // clamping: the prefix table is padded past both detector edges.
                 Wg[g] = fmaf(z[g], fmaf(sgn[g], t0.y, t0.x), c0f);
                 bg[g] = (uint32_t)__float_as_int(__fadd_rd(Wg[g], 12582912.0f));  // vh + magic
+                CBCT_DCHECK(pad_lo - magic + (int)bg[g] >= 0 && pad_lo - magic + (int)bg[g] < nvq);
 #ifdef CBCT_BP_SINGLE
                 // P[vh] and P[vh+1] (the second load hits the line the first brought to L1)
                 P0[g] = __ldg(pyc + bg[g]);
@@ -457,6 +458,9 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
     __shared__ float2 s_t2[kChunk];
     __shared__ long long s_base[kChunk];
     __shared__ int s_fs[FLAT ? kChunk : 1];
+#ifdef CBCT_CHECKED
+    __shared__ int s_vuc[kChunk];
+#endif
     const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
     if (cell < 0) {
         if (partials && threadIdx.x == 0) partials[blockIdx.x] = 0.0;
@@ -519,6 +523,9 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
             s_t2[k] = make_float2((float)(Bl - Bi), (float)(Ba - Bi));
             s_base[k] = (long long)ce.vu * nvq + pad_lo - (long long)magic;
             if (FLAT) s_fs[k] = cols[ce.vu].flat_slab;
+#ifdef CBCT_CHECKED
+            s_vuc[k] = ce.vu;
+#endif
         }
         __syncthreads();
 #pragma unroll 2
@@ -534,6 +541,8 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
                 // rays entirely below z: rows under W(t_b) above the mid-plane, W(t_a) below
                 const float W = fmaf(zp[g], g < GS ? t0.x : t0.y, t2.x);
                 bg[g] = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));
+                CBCT_DCHECK(s_base[k] + (long long)bg[g] - (long long)s_vuc[k] * nvq >= 0 &&
+                            s_base[k] + (long long)bg[g] - (long long)s_vuc[k] * nvq < nvq);
                 const float2 py = __ldg(pyc + bg[g]);
                 P0[g] = py.x;
                 P1[g] = py.y;

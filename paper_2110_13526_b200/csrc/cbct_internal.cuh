@@ -22,6 +22,26 @@
         if (_e != cudaSuccess) return cbct_fail_cuda(_e, #expr); \
     } while (0)
 
+// Checked build (make CHECKED=1 -> build-checked/libcbct_checked.so, loaded with CBCT_LIBRARY):
+// device-side bounds checks on the gathers and shared-memory indexing of the hot kernels, the
+// substitute for compute-sanitizer (closed on this GPU pool).  A failed check prints the
+// condition and traps; the default build compiles them out.
+#ifdef CBCT_CHECKED
+#include <cstdio>
+#define CBCT_DCHECK(cond)                                                                         \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("CBCT_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,       \
+                   (int)blockIdx.x, (int)threadIdx.x, #cond);                                     \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define CBCT_DCHECK(cond) \
+    do {                  \
+    } while (0)
+#endif
+
 int cbct_fail_cuda(cudaError_t e, const char* what);
 int cbct_fail(int code, const char* msg);
 void cbct_count_launch(int n = 1);

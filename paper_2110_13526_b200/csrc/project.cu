@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             const int2 sl = chunk_slabs(i == 0 ? h.tau_start : s_ent[m0 - 1].x, s_ent[m0 + cnt - 1].x, tref, wlo,
                                         whi, lo2f, ip2, nz);
             const int lo4 = sl.x & ~3, hi4 = (sl.y + 4) & ~3;
+            CBCT_DCHECK(m0 + cnt <= M && M <= ent_cap && lo4 >= 0 && hi4 <= zs && lo4 < hi4);
             const uint32_t bytes = (uint32_t)(hi4 - lo4) * 4u;
             float* dst = ring + (size_t)slot * slot_elems + RZ * zs + lo4;
             if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * bytes);
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             {
                 const int2 sl = chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
                 const int zs2 = zs >> 1;
+                CBCT_DCHECK(sl.x >= 0 && sl.y < zs && sl.x <= sl.y);
                 float2* col2 = reinterpret_cast<float2*>(stage + RZ * zs);
                 for (int pi = (sl.x >> 1) + threadIdx.x; pi <= (sl.y >> 1); pi += nct) {
                     float2 q = make_float2(0.0f, 0.0f);
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                     const float f = (s.tz - sB[m]) * sInv[m];
                     const float* q1 = stage + (m + RZ) * zs;  // Qc[m+1]
                     const int izn = s.iz + s.dz;
+                    CBCT_DCHECK(m >= 0 && m < cnt && s.iz >= 0 && s.iz < zs && izn >= 0 && izn < zs);
                     float a0, b0;
                     if (ZR) {
                         a0 = q1[s.iz - zs];
@@ -452,6 +455,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
                     s.jf += 1.0f;
                     s.tz = s.jf < s.kf ? fmaf(s.jf, s.dtz, s.tz0) : INFINITY;
                 }
+                CBCT_DCHECK(s.iz >= 0 && s.iz < zs);
                 s.acc += last[s.iz];
             }
             chunk_start = cend;
