@@ -509,7 +509,7 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         // 3 CTAs per SM (measured: config 2 16+zr 10.3 ms, 16 11.1 ms, 8 14.6 ms; config 3
         // 16 85 ms, 16+zr 103 ms, 12+zr 92 ms)
         auto qsm = [&](int cc, int zr) {
-            return 32 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + 3 * (2 * cc + 33) * 4;
+            return 48 + (p->max_intervals + 3) * 8 + per_c * (cc + zr) + 3 * (2 * cc + 33) * 4;
         };
         // C = 16 unless two CTAs of it no longer fit an SM's shared memory (zs >~ 800 slabs, i.e.
         // config 5's 1024 slabs: C=16 1514 ms with one CTA per SM, C=8 1279 ms with two; config

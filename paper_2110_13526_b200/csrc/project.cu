@@ -302,18 +302,24 @@ __device__ __forceinline__ int2 chunk_slabs(float tau_a, float tau_b, float tref
     return make_int2(min(max(ilo, CBCT_ZPAD - 1), CBCT_ZPAD + nz), min(max(ihi, CBCT_ZPAD - 1), CBCT_ZPAD + nz));
 }
 
-template <int RPT, int C, bool ZR>
+// ZS > 0: the slab stride zs as a compile-time constant (the BASELINE sizes and the parity
+// subsets), so phase 1 runs fully unrolled over a full chunk with immediate row offsets and the
+// chunk's dtau in registers; ZS = 0 keeps the runtime stride.  prod_hint > 0: the producer waits
+// on a drained slot with a hardware suspend hint instead of nanosleep polling.
+template <int RPT, int C, bool ZR, int ZS>
 __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restrict__ cols,
                                                    const int64_t* __restrict__ col_off,
                                                    const float2* __restrict__ col_ent, const double* __restrict__ wtab,
                                                    const float* __restrict__ vol, float* __restrict__ proj,
-                                                   double* __restrict__ partials, int nv, int nz, int zs, double lo2,
+                                                   double* __restrict__ partials, int nv, int nz, int zs_rt, double lo2,
                                                    double p2, int flat_v, int ent_cap, int64_t c0, int nu,
-                                                   int nviews) {
+                                                   int nviews, uint32_t prod_hint) {
+    const int zs = ZS > 0 ? ZS : zs_rt;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [2]
     uint64_t* empty = full + 2;                               // [2]
-    float2* s_ent = reinterpret_cast<float2*>(smem_raw + 32);
+    int2* s_win = reinterpret_cast<int2*>(smem_raw + 32);     // [2] staged slab window of each slot's chunk
+    float2* s_ent = reinterpret_cast<float2*>(smem_raw + 48);
     // ZR: [2][C+1][zs], row 0 of a slot is Qc[0] = 0 (never written after init) and rows
     // 1..cnt receive the staged cell columns; !ZR: [2][C][zs] (one row less per slot, when the
     // extra rows would cost a resident CTA) and Qc[0] = 0 is a predicated load.  Phase 1 turns
@@ -356,7 +362,10 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
         // stage only the 16-B-aligned slab window the chunk's rays can reach (the cone bound)
         for (int i = 0; i < nch; ++i) {
             const int slot = i & 1, round = i >> 1;
-            if (round > 0) mbar_wait_backoff(&empty[slot], (round - 1) & 1);
+            if (round > 0) {
+                if (prod_hint) mbar_wait_hint(&empty[slot], (round - 1) & 1, prod_hint);
+                else mbar_wait_backoff(&empty[slot], (round - 1) & 1);
+            }
             const int m0 = i * C, cnt = min(C, M - m0);
             const int2 sl = chunk_slabs(i == 0 ? h.tau_start : s_ent[m0 - 1].x, s_ent[m0 + cnt - 1].x, tref, wlo,
                                         whi, lo2f, ip2, nz);
@@ -364,7 +373,10 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             CBCT_DCHECK(m0 + cnt <= M && M <= ent_cap && lo4 >= 0 && hi4 <= zs && lo4 < hi4);
             const uint32_t bytes = (uint32_t)(hi4 - lo4) * 4u;
             float* dst = ring + (size_t)slot * slot_elems + RZ * zs + lo4;
-            if (lane == 0) mbar_arrive_expect_tx(&full[slot], cnt * bytes);
+            if (lane == 0) {
+                s_win[slot] = sl;  // released to the consumers by the arrive below
+                mbar_arrive_expect_tx(&full[slot], cnt * bytes);
+            }
             __syncwarp();
             for (int j = lane; j < cnt; j += 32)
                 bulk_g2s(dst + (size_t)j * zs, vol + (uint32_t)(__float_as_int(s_ent[m0 + j].y) + lo4), bytes,
@@ -406,20 +418,38 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
             // exactly that window).
             float* stage = ring + (size_t)slot * slot_elems;
             {
-                const int2 sl = chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
+                const int2 sl = ZS > 0 ? s_win[slot] : chunk_slabs(chunk_start, cend, tref, wlo, whi, lo2f, ip2, nz);
                 const int zs2 = zs >> 1;
                 CBCT_DCHECK(sl.x >= 0 && sl.y < zs && sl.x <= sl.y);
                 float2* col2 = reinterpret_cast<float2*>(stage + RZ * zs);
-                for (int pi = (sl.x >> 1) + threadIdx.x; pi <= (sl.y >> 1); pi += nct) {
-                    float2 q = make_float2(0.0f, 0.0f);
-                    float2* cp = col2 + pi;
+                if (ZS > 0 && cnt == C) {
+                    // full chunk: C rows at compile-time offsets, dtau in registers
+                    float dl[C];
+#pragma unroll
+                    for (int j = 0; j < C; ++j) dl[j] = sDl[j];
+                    for (int pi = (sl.x >> 1) + threadIdx.x; pi <= (sl.y >> 1); pi += nct) {
+                        float2 q = make_float2(0.0f, 0.0f);
+                        float2* cp = col2 + pi;
+#pragma unroll
+                        for (int j = 0; j < C; ++j) {
+                            const float2 x = cp[j * (ZS / 2)];
+                            q.x = fmaf(dl[j], x.x, q.x);
+                            q.y = fmaf(dl[j], x.y, q.y);
+                            cp[j * (ZS / 2)] = q;
+                        }
+                    }
+                } else {
+                    for (int pi = (sl.x >> 1) + threadIdx.x; pi <= (sl.y >> 1); pi += nct) {
+                        float2 q = make_float2(0.0f, 0.0f);
+                        float2* cp = col2 + pi;
 #pragma unroll 4
-                    for (int j = 0; j < cnt; ++j) {
-                        const float dl = sDl[j];
-                        const float2 x = cp[j * zs2];
-                        q.x = fmaf(dl, x.x, q.x);
-                        q.y = fmaf(dl, x.y, q.y);
-                        cp[j * zs2] = q;
+                        for (int j = 0; j < cnt; ++j) {
+                            const float dl = sDl[j];
+                            const float2 x = cp[j * zs2];
+                            q.x = fmaf(dl, x.x, q.x);
+                            q.y = fmaf(dl, x.y, q.y);
+                            cp[j * zs2] = q;
+                        }
                     }
                 }
             }
@@ -498,30 +528,51 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
         const int Cq = p->proj_q_c;
         const int ent_cap = (int)((p->max_intervals + 3) / 2 * 2);  // even: keeps the TMA ring 16-B aligned
         const int zr = p->proj_q_zr;
-        const size_t smem = 32 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * (Cq + zr) * p->zs * 4 +
+        const size_t smem = 48 + (size_t)ent_cap * sizeof(float2) + (size_t)2 * (Cq + zr) * p->zs * 4 +
                             (size_t)3 * (2 * Cq + 33) * 4;
         const int nt = p->proj_threads + 32;
-#define LAUNCH_Q2(R, CC, Z)                                                                                    \
+        // compile-time slab strides: BASELINE configs 1/2/3/5 (zs = 72/264/520/1032) and 32-slice subsets (40)
+        static const int zs_ct_off = getenv("CBCT_PROJ_ZS_RT") != nullptr;
+        const int zsc = zs_ct_off ? 0 : (int)p->zs;
+        static const uint32_t hint = getenv("CBCT_PROJ_HINT") ? (uint32_t)atoi(getenv("CBCT_PROJ_HINT")) : 0u;
+#define LAUNCH_Q3(R, CC, Z, ZSV)                                                                               \
         do {                                                                                                   \
-            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC, Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                            (int)smem));                                                       \
-            k_project_q<R, CC, Z><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w, vol,    \
-                                                         proj, partials, (int)p->nv, (int)p->nz, (int)p->zs,    \
-                                                         p->lo[2], p->pitch[2], p->flat_v, ent_cap, c0,         \
-                                                         (int)p->nu, (int)(view1 - view0));                     \
+            CBCT_CHECK(cudaFuncSetAttribute(k_project_q<R, CC, Z, ZSV>,                                        \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));          \
+            k_project_q<R, CC, Z, ZSV><<<grid, nt, smem, s>>>(p->d_cols, p->d_col_off, p->d_col_ent, p->d_w,   \
+                                                              vol, proj, partials, (int)p->nv, (int)p->nz,     \
+                                                              (int)p->zs, p->lo[2], p->pitch[2], p->flat_v,    \
+                                                              ent_cap, c0, (int)p->nu, (int)(view1 - view0),   \
+                                                              hint);                                           \
+        } while (0)
+#define LAUNCH_Q2(R, CC, Z) LAUNCH_Q3(R, CC, Z, 0)
+#define LAUNCH_Q2Z(R, CC, Z)                                                                                   \
+        do {                                                                                                   \
+            switch (zsc) {                                                                                     \
+                case 40: LAUNCH_Q3(R, CC, Z, 40); break;                                                       \
+                case 72: LAUNCH_Q3(R, CC, Z, 72); break;                                                       \
+                case 264: LAUNCH_Q3(R, CC, Z, 264); break;                                                     \
+                case 520: LAUNCH_Q3(R, CC, Z, 520); break;                                                     \
+                case 1032: LAUNCH_Q3(R, CC, Z, 1032); break;                                                   \
+                default: LAUNCH_Q3(R, CC, Z, 0); break;                                                        \
+            }                                                                                                  \
         } while (0)
 #define LAUNCH_Q(R, CC)                                                                                        \
         do {                                                                                                   \
             if (zr) LAUNCH_Q2(R, CC, true); else LAUNCH_Q2(R, CC, false);                                      \
+        } while (0)
+#define LAUNCH_QZ(R, CC)                                                                                       \
+        do {                                                                                                   \
+            if (zr) LAUNCH_Q2Z(R, CC, true); else LAUNCH_Q2Z(R, CC, false);                                    \
         } while (0)
         switch (p->proj_rpt * 100 + Cq) {
             case 108: LAUNCH_Q(1, 8); break;
             case 112: LAUNCH_Q(1, 12); break;
             case 116: LAUNCH_Q(1, 16); break;
             case 132: LAUNCH_Q(1, 32); break;
-            case 208: LAUNCH_Q(2, 8); break;
+            case 208: LAUNCH_QZ(2, 8); break;
             case 212: LAUNCH_Q(2, 12); break;
-            case 216: LAUNCH_Q(2, 16); break;
+            case 216: LAUNCH_QZ(2, 16); break;
             case 232: LAUNCH_Q(2, 32); break;
             case 408: LAUNCH_Q(4, 8); break;
             case 412: LAUNCH_Q(4, 12); break;
@@ -529,7 +580,10 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
             default: LAUNCH_Q(4, 32); break;
         }
 #undef LAUNCH_Q
+#undef LAUNCH_QZ
 #undef LAUNCH_Q2
+#undef LAUNCH_Q2Z
+#undef LAUNCH_Q3
         CBCT_CHECK(cudaGetLastError());
         cbct_count_launch();
         return 0;

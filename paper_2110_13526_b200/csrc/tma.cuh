@@ -57,6 +57,21 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
     }
 }
 
+// Producer-side wait with a suspend-time hint: try_wait may suspend the warp in hardware until
+// the phase completes or hint_ns elapse, instead of polling with nanosleep (each poll is three
+// issued instructions taken from the consumer warps of the SM).
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITH_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITH_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+
 // 1-D bulk copy global -> shared (TMA engine); bytes % 16 == 0, both addresses 16-B aligned.
 // Completion is signalled on `bar` as transaction bytes.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
