@@ -114,13 +114,17 @@ class ClockSampler:
 
 
 def committed_traffic(cfg: int) -> dict:
-    """DRAM bytes per operator application of the hot kernels from the committed ncu captures
-    (profiles/traffic_r1.json)."""
-    try:
-        with open(ROOT / "profiles" / "traffic_r1.json") as f:
-            return json.load(f).get(f"config{cfg}", {})
-    except (OSError, ValueError):
-        return {}
+    """DRAM bytes per operator application of the hot kernels from the committed ncu captures of
+    this build (profiles/traffic_r2.json; round-1 file as a fallback)."""
+    for name in ("traffic_r2.json", "traffic_r1.json"):
+        try:
+            with open(ROOT / "profiles" / name) as f:
+                d = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if f"config{cfg}" in d:
+            return dict(d[f"config{cfg}"], source=d.get("source"))
+    return {}
 
 
 # ------------------------------------------------------------------ CPU legs --
@@ -393,7 +397,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     dom, t_dom = ("A^T", t_at) if t_at >= t_a else ("A", t_a)
     achieved = SLOTS_PER_NNZ * nnz / (t_dom * 1e-3)
     f32 = args.precision == "f32"
-    kname = {"A^T": "k_bp_boundary" if f32 else "k_bp64", "A": "k_project_q" if f32 else "k_project64"}[dom]
+    bp_kernel = "k_bp_sided" if op.info.bp_sided_gs > 0 else "k_bp_boundary"
+    kname = {"A^T": bp_kernel if f32 else "k_bp64", "A": "k_project_q" if f32 else "k_project64"}[dom]
     traffic = committed_traffic(cfg) if f32 else {}
     roof = {"bound": "issue", "kernel": f"{dom} ({kname})",
             "achieved": achieved / 1e9, "peak": peak_slots / 1e9, "unit": "Gslot/s", "frac": achieved / peak_slots,
@@ -411,6 +416,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "definition": "SURVEY.md 8(d): 8 FP32-lane-slot equivalents per nonzero of A; peak = 148 SM x 128 "
                           f"lanes x f_SM (median SM clock under load, {f_mhz:.0f} MHz)",
             "ncu_utilisation": {k: v for k, v in traffic.get("ncu_utilisation", {}).items() if k != "source"} or None,
+            "algorithmic_bytes": 4 * (op.n + op.m),
             "frac_A": SLOTS_PER_NNZ * nnz / (t_a * 1e-3) / peak_slots,
             "frac_AT": SLOTS_PER_NNZ * nnz / (t_at * 1e-3) / peak_slots}
     cpu = None
