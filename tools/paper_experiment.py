@@ -31,13 +31,14 @@ def run(op, b, method, K, **kw):
             "iters_to_1pct": iterations_to_tolerance(rep.history, 0.01)}
 
 
-def case(name, vg, tr, psirt_cap):
-    op = P.CbctOperator(vg, tr)
+def case(name, vg, tr, psirt_cap, precision="f32"):
+    op = P.CbctOperator(vg, tr, precision=precision)
     x = op.phantom_internal(P.shepp_logan_3d())
     b_int = op.new_projections()
     op.project_internal(x, b_int)
     b = InternalProjections(tr, b_int)
-    out = {"geometry": f"{vg.nx}x{vg.ny}x{vg.nz}, {tr.n_views} views of {tr.detector.nu}x{tr.detector.nv}"}
+    out = {"geometry": f"{vg.nx}x{vg.ny}x{vg.nz}, {tr.n_views} views of {tr.detector.nu}x{tr.detector.nv}",
+           "precision": precision}
     out["cgls_40"] = run(op, b, "cgls", 40)
     out["psirt_to_1pct"] = run(op, b, "psirt", psirt_cap, rel_discrepancy_tol=0.01)
     out["psirt_40"] = run(op, b, "psirt", 40)
@@ -54,6 +55,7 @@ def main():
 
     vg, tr = geom_from_golden(load_golden("desk"))  # the reference's configs/desk_scale.cfg geometry
     doc["desk"] = case("desk", vg, tr, 1500)
+    doc["desk_f64"] = case("desk_f64", vg, tr, 1500, precision="f64")
     vg, tr = bench.geometry(3)
     doc["config3"] = case("config3", vg, tr, 400)
     out = pathlib.Path(sys.argv[1]) if len(sys.argv) > 1 else None

@@ -33,7 +33,11 @@ def t(fn):
     return s.elapsed_time(e) / reps
 
 
-only = sys.argv[3] if len(sys.argv) > 3 else ""  # "A" or "AT": time one operator only
+only = sys.argv[3] if len(sys.argv) > 3 else ""  # "A" or "AT": time one operator only; "D": diag(A^T A)
+if only == "D":
+    td = t(lambda: op.backproject_internal(None, r, mode=2))
+    print(f"cfg{cfg} {os.environ.get('PREC', 'f32')}: diag(A^T A) {td:.3f} ms", flush=True)
+    sys.exit(0)
 ta = t(lambda: op.project_internal(x, p)) if only != "AT" else float("nan")
 tat = t(lambda: op.backproject_internal(y, r, scratch=scr)) if only != "A" else float("nan")
 N, V = vg.nx, tr.n_views
