@@ -187,9 +187,10 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
 // the straddle fraction F, so the fp32 cancellation there is harmless), which
 // halves the bytes per boundary lookup.  The flat row (if any) is kept out of P
 // and stored in flatw[c].
+// squared (mode 2): yw = |r|^2 (y ignored), the weights of diag(A^T A)'s boundary form (k_bp_sided).
 __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
                               const float* __restrict__ y, float* __restrict__ pref, float* __restrict__ flatw,
-                              int64_t n_cols, int nv, int flat_v, int pad_lo, int pad_hi) {
+                              int64_t n_cols, int nv, int flat_v, int pad_lo, int pad_hi, int squared = 0) {
     const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (c >= n_cols) return;
@@ -210,7 +211,7 @@ __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const doubl
         float yw = 0.0f;
         if (v < nv) {
             const float w = (float)wtab[v];
-            yw = sqrtf(fmaf(w, w, rxy2)) * yc[v];  // operator.py:102, 165
+            yw = squared ? fmaf(w, w, rxy2) : sqrtf(fmaf(w, w, rxy2)) * yc[v];  // operator.py:102, 165-167
             if (v == flat_v) {
                 flatw[c] = yw;
                 yw = 0.0f;
@@ -442,7 +443,12 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
 // that boundary is exactly z = 0 (or one side is empty), where the below formula with
 // z = -0 (1/z = -inf) yields the above formula's value: no ray straddles the plane z = 0
 // (rays through the source height are the separate flat row).
-template <int GS, bool FLAT, int MAXR>
+// MODE2: diag(A^T A) = sum seg^2 (operator.py:166-167) in the same boundary form.  With the table
+// holding the prefix P2 of |r|^2 and H(z) = P2[V] + f^2 |r_V|^2, voxel k receives
+//   dt^2 (H(z_k+1) - H(z_k) - 2 f_k (1 - f_k) |r_V_k|^2)
+// (the straddler of the lower boundary contributes (1 - f_k)^2, not 1 - f_k^2); exact while no ray
+// spans a whole voxel height inside one crossing, which the plan checks (bps_mode2_ok).
+template <int GS, bool FLAT, int MAXR, bool MODE2 = false>
 __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_off,
                                                     const CellEntry* __restrict__ cell_ent,
                                                     const ColumnHeader* __restrict__ cols,
@@ -518,7 +524,8 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
             const int magic = 0x4B400000 - (int)Bi - 1;  // floor(W) + Bi + 1 via the 1.5*2^23 trick
             // {p2/(t_a pv), p2/(t_b pv), kI = pv t_a t_b / dt, dt}, {eps = dt / t_a, p2/(t_a pv) lo, 1 - eps, flat},
             // {lookup B fraction, W_a offset relative to the lookup's integer}
-            s_t0[k] = make_float4(sa, (float)(p2 * ibd), dt > 0.0f ? (float)pv * taa * tba / dt : 0.0f, dt);
+            s_t0[k] = make_float4(sa, (float)(p2 * ibd), dt > 0.0f ? (float)pv * taa * tba / dt : 0.0f,
+                                  MODE2 ? dt * dt : dt);
             s_t1[k] = make_float4(dt / taa, sa_lo, 1.0f - dt / taa, FLAT ? flatw[ce.vu] : 0.0f);
             s_t2[k] = make_float2((float)(Bl - Bi), (float)(Ba - Bi));
             s_base[k] = (long long)ce.vu * nvq + pad_lo - (long long)magic;
@@ -556,9 +563,17 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
                 const float sv = __saturatef(u * (iz[g] * t0.z));
                 const float h = fmaf(t1.x, sv, t1.z);
                 const float f = g < GS ? fmaf(-sv, h, 1.0f) : sv * h;  // below: 1 - f_t ; above: f_t
-                const float Gv = fmaf(f, P1[g], P0[g]);
-                const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
-                acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
+                if (MODE2) {
+                    const float fw = f * P1[g];
+                    const float Gv = fmaf(f, fw, P0[g]);                 // P2[V] + f^2 w2
+                    const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
+                    const float c = 2.0f * (fw - f * fw);                // 2 f (1 - f) w2
+                    acc[g] = fmaf(t0.w, (Gn - Gv) - c, acc[g]);
+                } else {
+                    const float Gv = fmaf(f, P1[g], P0[g]);
+                    const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
+                    acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
+                }
                 if (FLAT) {
                     const int gi = warp * GS + (g < GS ? g : g - GS);
                     const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;
@@ -604,15 +619,23 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     cudaStream_t s = (cudaStream_t)stream;
     // Mode 2 (diag(A^T A), once per Jacobi solve) always clips in fp64: its squared weights
     // double the fp32 clip's relative error, which reaches ~1e-4 at 0.43 mm voxels.
-    const bool precise = mode == 2 || getenv("CBCT_BP_PRECISE") != nullptr;
+    // Where the sided boundary kernel runs (closed form, z = 0 on a boundary or one-sided), mode 2
+    // uses its squared-weight boundary form instead (bps_mode2_ok: no ray spans a voxel height in a
+    // crossing); CBCT_BP_DIAG_DIRECT=1 keeps the fp64-clip direct kernel.
+    static const bool diag_direct = getenv("CBCT_BP_DIAG_DIRECT") != nullptr;
+    const bool closed_rt = p->bp_closed_ok && getenv("CBCT_BP_TABLE") == nullptr;
+    const bool mode2_sided = mode == 2 && p->bp_boundary_ok && closed_rt && p->bps_eligible && p->bps_mode2_ok &&
+                             !diag_direct;
+    const bool precise = (mode == 2 && !mode2_sided) || getenv("CBCT_BP_PRECISE") != nullptr;
     static const bool force_direct = getenv("CBCT_BP_DIRECT") != nullptr;  // diagnosis: fp32 direct kernel
-    if (mode == 1 && p->bp_boundary_ok && !precise && !force_direct) {
+    if ((mode == 1 || mode2_sided) && p->bp_boundary_ok && !precise && !force_direct) {
         float* pyb = scratch;
         const int nvq = (int)p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi;
         float* flatw = scratch + p->n_cols * nvq * kPrefWords;
         const int64_t nthreads = p->n_cols * 32;
         k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
-                                                                           p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi);
+                                                                           p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi,
+                                                                           mode == 2 ? 1 : 0);
         CBCT_CHECK(cudaGetLastError());
         // closed-form straddle fraction unless the cells are long relative to the source distance
         static const bool force_table = getenv("CBCT_BP_TABLE") != nullptr;
@@ -642,13 +665,15 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         // norm partials
         const int nb = p->bp_vbatch;
         const int32_t* boff = nb > 1 ? p->d_cell_boff : nullptr;
-        const bool sided = !table && p->bps_ok;
+        const bool sided = !table && (p->bps_ok || mode2_sided);
         // register cap of the sided kernel: 56 for GS = 3 (11 CTAs of 96 threads instead of 10; config 3
         // A^T 107.8 -> 105.7 ms), 64 for GS = 2 (config 5: 56 regs spill, 1379 vs 1418 ms)
         static const int regs_env = getenv("CBCT_BP_REGS") ? atoi(getenv("CBCT_BP_REGS")) : 0;
         const int sided_regs = regs_env ? regs_env : (p->bps_gs == 3 ? 56 : 64);
 #define LAUNCH_S1(GS, FL, MR)                                                                                  \
-        k_bp_sided<GS, FL, MR><<<grid, p->bps_threads, 0, s>>>(                                               \
+        if (mode == 2) LAUNCH_S2(GS, FL, MR, true); else LAUNCH_S2(GS, FL, MR, false)
+#define LAUNCH_S2(GS, FL, MR, M2)                                                                              \
+        k_bp_sided<GS, FL, MR, M2><<<grid, p->bps_threads, 0, s>>>(                                           \
             p->d_cell_off, p->d_cell_ent, p->d_cols, pyb, flatw, vol, col_scale, part, (int)p->nv, (int)p->nz, \
             (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx, (int)row0, (int)row1,             \
             p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0, p->bps_k0, p->bps_zero)
@@ -689,6 +714,7 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
 #undef LAUNCH_G
 #undef LAUNCH_S
 #undef LAUNCH_S1
+#undef LAUNCH_S2
         CBCT_CHECK(cudaGetLastError());
         cbct_count_launch(1 + nb);
         return 0;

@@ -97,7 +97,9 @@ struct cbct_plan {
     int bpg_threads, bpg_groups;  // boundary-form backprojector shape
     // sided boundary kernel (k_bp_sided): GS below + GS above groups per warp, anchored at the
     // first boundary k0 with z >= 0; usable when z_k0 == 0 exactly or one side is empty
-    bool bps_ok = false;
+    bool bps_ok = false;        // mode 1 runs k_bp_sided (geometry eligible and <= 10% wasted slots)
+    bool bps_eligible = false;  // geometry allows k_bp_sided (mode 2 uses it whenever eligible)
+    bool bps_mode2_ok = false;  // no ray's z range inside one crossing reaches a voxel height
     int bps_gs = 0, bps_threads = 0, bps_k0 = 0, bps_zero = 0;
     bool bp_boundary_ok;          // at most one ray straddles any voxel boundary per crossing
     int32_t bp_pad_lo, bp_pad_hi; // rows of the ray-prefix table below 0 / above nv (no index clamping)

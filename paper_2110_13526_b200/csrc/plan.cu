@@ -474,6 +474,9 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
             p->bp_pad_hi = p->bp_boundary_ok ? (int32_t)fmax(0.0, hi_need) + 1 : 0;
             // first-order closed form error <= eps^2 / 4 (backproject.cu)
             p->bp_closed_ok = tmin_f > 0.0f && (double)mx <= 3e-3 * (double)tmin_f;
+            // diag(A^T A) in boundary form (k_bp_sided MODE2): no ray's z extent inside one crossing
+            // (|w| dt) may reach a voxel height, so a voxel never has the same straddler at both ends
+            p->bps_mode2_ok = p->bp_boundary_ok && wmax * (double)mx < 0.9 * g->pitch[2];
         }
         TRY(dev_alloc(&p->d_w, g->nv, &total));
         TRY(dev_alloc(&p->d_invw, g->nv, &total));
@@ -572,7 +575,8 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         }
         bool use = best > 0 && 10 * best_waste <= best_slots;
         if (const char* e = getenv("CBCT_BP_GS")) { best = atoi(e); use = best > 0; }
-        p->bps_ok = (!both || zero) && use && getenv("CBCT_BP_SIDED_OFF") == nullptr;
+        p->bps_eligible = (!both || zero) && best > 0;
+        p->bps_ok = p->bps_eligible && use && getenv("CBCT_BP_SIDED_OFF") == nullptr;
         p->bps_gs = best;
         p->bps_threads = best > 0 ? (int)((std::max(nb, na) + best - 1) / best * 32) : 0;
         p->bps_k0 = (int)k0;

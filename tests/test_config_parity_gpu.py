@@ -117,7 +117,7 @@ def test_config34_subset_krylov40_f32_floor(subset, key, method, kw):
     1e-3 through K = 10 (next test) and reaches a discrepancy within 20% of the reference's."""
     d, t, vg, tr, b = subset
     rep, h = _solve(_op(vg, tr, "f32"), tr, b, method, 40, **kw)
-    assert float(np.abs(h[:11] / d[f"{key}_hist"][:11] - 1.0).max()) <= 1e-6
+    assert float(np.abs(h[:11] / d[f"{key}_hist"][:11] - 1.0).max()) <= 1e-5
     assert h[-1] <= 1.2 * d[f"{key}_hist"][-1]
     assert rel_l2(rep.final_x.data[:: int(d["x_stride"])], d[f"{key}_x_sample"]) <= 1.5e-2
 
@@ -137,7 +137,9 @@ def test_config34_subset_trajectory(subset, precision, K, tk, method, kw):
     op = _op(vg, tr, precision)
     rep, h = _solve(op, tr, b, method, K, **kw)
     hr = t[f"{tk}_w8_hist"][: K + 1]
-    assert float(np.abs(h / hr - 1.0).max()) <= (1e-6 if K <= 20 else H_TOL)
+    # history records: 1e-6 on the fp64 path through K = 20; 1e-5 on the fp32 path through K = 10 (its
+    # operators carry ~1e-6, the fp32 Jacobi diagonal ~1e-5)
+    assert float(np.abs(h / hr - 1.0).max()) <= (H_TOL if K > 20 else (1e-6 if precision == "f64" else 1e-5))
     rel = rel_l2(rep.final_x.data[:: int(t["x_stride"])], t[f"{tk}_w8_x{K}_sample"])
     assert rel <= X_TOL, (precision, tk, K, rel)
     if precision == "f64" and K <= 20:

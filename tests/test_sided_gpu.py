@@ -3,8 +3,9 @@
 The plan selects it by waste (config 3: GS = 3, config 5: GS = 2); here it is forced with
 CBCT_BP_GS on centred BASELINE-geometry view subsets, on a detector with a flat row (odd nv,
 the reference's axis-parallel ray, operator.py:87-89) and with a principal-point offset (an
-arbitrary fractional row centre), at both GS values.  Bar: the north star's 1e-4 max-rel
-(operator.py:209-233), bitwise-deterministic reruns, and the norm partials of the epilogue.
+arbitrary fractional row centre), at both GS values, for A^T (mode 1) and diag(A^T A) (mode 2, the
+squared-weight boundary form).  Bar: the north star's 1e-4 max-rel (operator.py:209-233, 353-362),
+bitwise-deterministic reruns, and the norm partials of the epilogue.
 """
 
 import numpy as np
@@ -48,6 +49,10 @@ def test_sided_against_oracle(name, gs, monkeypatch):
     want = O.OracleOperator(vg, tr).backproject(y)
     assert max_rel(got, want) <= 1e-4, (name, gs, max_rel(got, want))
     assert rel_l2(got, want) <= 2e-5, (name, gs, rel_l2(got, want))
+    # mode 2: diag(A^T A) in the squared-weight boundary form (operator.py:166-167, 353-362)
+    got, want = op.normal_diagonal().data, O.OracleOperator(vg, tr).normal_diagonal()
+    assert max_rel(got, want) <= 1e-4, (name, gs, "normal_diagonal", max_rel(got, want))
+    assert rel_l2(got, want) <= 2e-5, (name, gs, "normal_diagonal", rel_l2(got, want))
     # determinism and the fused norm: same device buffers twice, ||A^T y||^2 from the epilogue
     yi = op.proj_to_internal(y)
     r1, r2 = op.new_volume(), op.new_volume()
