@@ -176,22 +176,32 @@ def cpu_vector_time(cfg: int):
 
 def cpu_views(cfg: int, threads: int) -> int:
     """Sample size: enough views that the worker-parallel backprojector uses every host thread
-    (its parallelism is min(workers, threads), operator.py:219), at most the whole trajectory."""
+    (its parallelism is min(workers, threads), operator.py:219) and that the k -> 2k difference
+    (32+ views of traversal) stands clear of the run-to-run noise of A^T's fixed cost."""
     V = CONFIGS[cfg][1]
-    return max(1, min(V, threads, 32))
+    return max(1, min(V // 2, max(threads, 32)))
+
+
+def cpu_workers(cfg: int, threads: int, k: int) -> int:
+    """Backprojector workers as the reference deals them (operator.py:219-220): all threads, capped
+    so the W private fp64 accumulators stay within 64 GB of host memory."""
+    N = CONFIGS[cfg][0]
+    return max(1, min(threads, k, int(64e9 // (8 * N ** 3))))
 
 
 def cpu_extrapolate(cfg: int, k: int, t1, t2):
-    """Per-view slope and fixed cost from samples at k and 2k views (same worker count):
-    t(v) = F + v s  ->  full = F + V s.  The A^T fixed cost (the W private accumulators'
-    allocation and their serial merge, operator.py:222-233) is counted once, not V/k times."""
+    """Time of one full-trajectory A and A^T from samples at k and 2k views with the same worker
+    count: t(v) = F + v s  ->  full = F + V s, so the fixed cost F is counted once.  A^T's F is
+    the W private accumulators' allocation, first-touch page faults and serial merge
+    (operator.py:222-233); A has none.  t1 / t2: (t_A, t_AT) medians at k and 2k views."""
     V = CONFIGS[cfg][1]
     out = {}
     for name, a, b in (("t_A", t1[0], t2[0]), ("t_AT", t1[1], t2[1])):
-        slope = max((b - a) / k, 0.0)
-        fixed = max(a - k * slope, 0.0)
-        if slope == 0.0:  # timing noise: fall back to proportional scaling
-            slope, fixed = a / k, 0.0
+        slope = (b - a) / k
+        if slope <= 0.0:  # noise swamped the difference: scale the 2k sample proportionally
+            slope, fixed = b / (2 * k), 0.0
+        else:
+            fixed = max(a - k * slope, 0.0)
         out[name] = fixed + V * slope
         out[name + "_fixed"] = fixed
     return out
@@ -199,24 +209,26 @@ def cpu_extrapolate(cfg: int, k: int, t1, t2):
 
 def cpu_sample(cfg: int, threads: int = 0):
     """CPU time of one CGLS iteration of the reference algorithm (one A + one A^T + the vector
-    updates) on this host, extrapolated from two view samples (k and 2k views)."""
+    updates) on this host, extrapolated from view samples at k and 2k views."""
     from oracle import oracle as O
 
     threads = int(O.lib().oracle_max_threads()) if threads < 1 else threads
     V = CONFIGS[cfg][1]
     k = cpu_views(cfg, threads)
-    workers = min(threads, k)
+    workers = cpu_workers(cfg, threads, k)
     t1 = cpu_time_views(cfg, k, workers, threads)
     if 2 * k <= V:
         t2 = cpu_time_views(cfg, 2 * k, workers, threads)
         ex = cpu_extrapolate(cfg, k, t1, t2)
-        how = f"A and A^T timed on {k} and {2 * k} of {V} views, per-view slope x {V} + fixed cost"
+        how = (f"A and A^T timed on {k} and {2 * k} of {V} views (t_A {t1[0]:.2f}/{t2[0]:.2f} s, "
+               f"t_AT {t1[1]:.2f}/{t2[1]:.2f} s); full = fixed cost + {V} x per-view slope")
     else:
         ex = {"t_A": t1[0] * V / k, "t_AT": t1[1] * V / k, "t_A_fixed": 0.0, "t_AT_fixed": 0.0}
         how = f"A and A^T on all {V} views"
     tv = cpu_vector_time(cfg)
     return {**ex, "t_vec": tv, "t_iter": ex["t_A"] + ex["t_AT"] + tv, "views_sampled": k, "workers": workers,
-            "threads": threads, "sample": how + "; vector updates at full size (numpy fp64)", "extrapolated": k < V}
+            "threads": threads, "sample": how + f"; workers {workers}; vector updates at full size (numpy fp64)",
+            "extrapolated": k < V}
 
 
 def run_reference(args, cfg, rank, world):
@@ -231,20 +243,24 @@ def run_reference(args, cfg, rank, world):
     threads = int(O.lib().oracle_max_threads())
     N, V, nu, nv, solver, K = CONFIGS[cfg]
     k = cpu_views(cfg, threads)
-    workers = min(threads, k)
+    workers = cpu_workers(cfg, threads, k)
     for _ in range(args.warmup):
         cpu_time_views(cfg, k, workers)
     samples = [cpu_time_views(cfg, k, workers) for _ in range(args.steps)]
     t1 = (float(np.median([s[0] for s in samples])), float(np.median([s[1] for s in samples])))
     if 2 * k <= V:
-        ex = cpu_extrapolate(cfg, k, t1, cpu_time_views(cfg, 2 * k, workers))
+        s2 = [cpu_time_views(cfg, 2 * k, workers) for _ in range(2)]
+        t2 = (float(np.median([s[0] for s in s2])), float(np.median([s[1] for s in s2])))
+        ex = cpu_extrapolate(cfg, k, t1, t2)
     else:
+        t2 = None
         ex = {"t_A": t1[0] * V / k, "t_AT": t1[1] * V / k, "t_A_fixed": 0.0, "t_AT_fixed": 0.0}
     t_iter = ex["t_A"] + ex["t_AT"] + cpu_vector_time(cfg)
     val = 1.0 / t_iter
-    sample = (f"A and A^T of the reference algorithm on {k} of {V} views (median of {args.steps} steps) and once "
-              f"on {2 * k} views; iteration = fixed cost + {V} x per-view slope; workers {workers}, "
-              f"{threads} OpenMP threads; vector updates at full size (numpy fp64)")
+    sample = (f"A and A^T of the reference algorithm on {k} of {V} views (median of {args.steps} steps: t_A "
+              f"{t1[0]:.2f} s, t_AT {t1[1]:.2f} s) and on {2 * k} views (median of 2"
+              + (f": t_A {t2[0]:.2f} s, t_AT {t2[1]:.2f} s" if t2 else "") + f"); iteration = fixed cost + {V} x "
+              f"per-view slope; workers {workers}, {threads} OpenMP threads; vector updates at full size (numpy fp64)")
     line = {
         "impl": "reference", "metric": "CGLS iterations/sec", "value": val, "unit": "it/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_iter * 1e3, "higher_is_better": True,
