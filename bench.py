@@ -262,14 +262,16 @@ def run_reference(args, cfg, rank, world):
     val = 1.0 / t_iter
     sample = (f"A and A^T of the reference algorithm on {k} of {V} views (median of {n_samples} samples: t_A "
               f"{t1[0]:.2f} s, t_AT {t1[1]:.2f} s) and on {2 * k} views (median of 2"
-              + (f": t_A {t2[0]:.2f} s, t_AT {t2[1]:.2f} s" if t2 else "") + f"); iteration = fixed cost + {V} x "
+              + (f": t_A {t2[0]:.2f} s, t_AT {t2[1]:.2f} s" if t2 else "") + f"); iteration (one A + one A^T + the vector updates, as every solver's step) = fixed cost + {V} x "
               f"per-view slope; workers {workers}, {threads} OpenMP threads; vector updates at full size (numpy fp64)")
+    solver = args.solver or CONFIGS[cfg][4]
+    sname = SOLVER_NAME[solver]
     line = {
-        "impl": "reference", "metric": "CGLS iterations/sec", "value": val, "unit": "it/s", "n_gpus": world,
+        "impl": "reference", "metric": f"{sname} iterations/sec", "value": val, "unit": "it/s", "n_gpus": world,
         "steps": n_samples, "warmup": args.warmup, "ms_per_step": t_iter * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, CGLS step",
-                   "parallelism": "cpu-openmp"},
+        "config": {"workload": f"config{cfg}: Shepp-Logan {N}^3, {V} views of {nu}x{nv}, {sname} step",
+                   "solver": solver, "precision": "f64", "parallelism": "cpu-openmp"},
         "gups_A": N ** 3 * V / ex["t_A"] / 1e9, "gups_AT": N ** 3 * V / ex["t_AT"] / 1e9,
         "t_A_s": ex["t_A"], "t_AT_s": ex["t_AT"], "t_AT_fixed_s": ex["t_AT_fixed"],
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port", "sample": sample,
