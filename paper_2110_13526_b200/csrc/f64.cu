@@ -407,6 +407,7 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
     const int ne = (int)(cell_off[cell + 1] - off);
     for (int k = threadIdx.x; k < nv; k += blockDim.x)
         s_irz[k] = fabs(wtab[k]) < 1e-12 * g.p2 ? 0.0 : 1.0 / wtab[k];
+    const double ipv = 1.0 / pv;
     double z0[ZPT], z1[ZPT], acc[ZPT];
     int iz[ZPT];
 #pragma unroll
@@ -432,12 +433,14 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
 #pragma unroll
             for (int r = 0; r < ZPT; ++r) {
                 if (iz[r] >= nz) continue;
-                // candidate rows from the direct plane parameters, one row of margin
+                // candidate rows from the direct plane parameters: a ray can meet the voxel inside the
+                // crossing only if its row lies in [vmin, vmax]; 1e-6 rows of margin cover the
+                // rounding of these bounds (the exact clip below decides)
                 const double qa0 = z0[r] * ia, qb0 = z0[r] * ib, qa1 = z1[r] * ia, qb1 = z1[r] * ib;
-                const double vmin = (fmin(fmin(qa0, qb0), fmin(qa1, qb1)) - det00z) / pv;
-                const double vmax = (fmax(fmax(qa0, qb0), fmax(qa1, qb1)) - det00z) / pv;
-                const int va = max(0, (int)floor(vmin) - 1);
-                const int vb = min(nv - 1, (int)ceil(vmax) + 1);
+                const double vmin = (fmin(fmin(qa0, qb0), fmin(qa1, qb1)) - det00z) * ipv;
+                const double vmax = (fmax(fmax(qa0, qb0), fmax(qa1, qb1)) - det00z) * ipv;
+                const int va = max(0, (int)ceil(vmin - 1e-6));
+                const int vb = min(nv - 1, (int)floor(vmax + 1e-6));
                 for (int v = va; v <= vb; ++v) {
                     const int64_t ray = rb + v;
                     const int2 is = iz_tab[ray];
