@@ -395,7 +395,6 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
                                               const double* __restrict__ col_scale, double* __restrict__ partials,
                                               Grid3 g, int nv, double det00z, double pv, int mode, int row0,
                                               int row1) {
-    extern __shared__ double s_irz[];  // 1/rz per row (0 for a flat row)
     __shared__ Cross s_x[kChunk];
     const int nx = (int)g.n0, nz = (int)g.n2;
     const int64_t cell = tiled_cell(blockIdx.x, nx, row0, row1);
@@ -405,8 +404,6 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    for (int k = threadIdx.x; k < nv; k += blockDim.x)
-        s_irz[k] = fabs(wtab[k]) < 1e-12 * g.p2 ? 0.0 : 1.0 / wtab[k];
     const double ipv = 1.0 / pv;
     double z0[ZPT], z1[ZPT], acc[ZPT];
     int iz[ZPT];
@@ -446,11 +443,6 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
                     const int2 is = iz_tab[ray];
                     const int d = (iz[r] - is.x) * is.y;  // z steps from the entry slab to this slab
                     if (is.y == 0 ? iz[r] != is.x : d < 0) continue;
-                    const double irz = s_irz[v];
-                    if (irz != 0.0) {  // cheap reject: direct z-plane parameters miss the crossing
-                        const double u1 = z0[r] * irz, u2 = z1[r] * irz;
-                        if (fmin(x.tb, fmax(u1, u2)) - fmax(x.ta, fmin(u1, u2)) < -1e-9 * x.tb) continue;
-                    }
                     const RayZ q = rz_tab[ray];
                     double t_in = -1e300, t_out = q.tz0;  // accumulated z planes (tz += dtz)
                     for (int j = 0; j < d; ++j) {
@@ -692,12 +684,9 @@ extern "C" int cbct_backproject_f64(const cbct_plan* p, const double* proj, doub
     if (!p->d_len64) return cbct_fail(CBCT_E_ARG, "cbct_backproject_f64: call cbct_plan_enable_f64 first");
     cudaStream_t s = (cudaStream_t)stream;
     const dim3 grid((unsigned)(((p->nx + 15) / 16) * ((p->ny + 15) / 16) * 256));
-    const size_t smem = (size_t)p->nv * sizeof(double);
 #define LAUNCH64(Z)                                                                                          \
     do {                                                                                                     \
-        if (smem > 40 * 1024)                                                                                \
-            CBCT_CHECK(cudaFuncSetAttribute(k_bp_f64<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        k_bp_f64<Z><<<grid, p->bp_threads, smem, s>>>(p->d_cell_off, p->d_cell_ent, (const double2*)p->d_cell_t64, \
+        k_bp_f64<Z><<<grid, p->bp_threads, 0, s>>>(p->d_cell_off, p->d_cell_ent, (const double2*)p->d_cell_t64, \
                                                       p->d_w, p->d_len64, (const RayZ*)p->d_rayz64,             \
                                                       (const int2*)p->d_rayiz64, proj, vol, col_scale, partials, \
                                                       grid3(p), (int)p->nv, p->det00z, p->pv, mode, 0,          \
