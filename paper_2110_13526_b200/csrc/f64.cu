@@ -137,7 +137,9 @@ __device__ double walk_ray(const Grid3& g, double sx, double sy, double sz, doub
 
 // y[c*nv + v] = walk of ray (view, u, v), c = view*nu + u; grid-stride over rays, so each
 // thread's rays and its partial of ||y||^2 are fixed by the launch shape (deterministic).
-__global__ void __launch_bounds__(256) k_project_f64(Grid3 g, const double* __restrict__ srcs,
+// Four CTAs per SM (64 registers): the walk is latency-bound on its volume loads and its fp64
+// dependency chain, so occupancy pays (config 3: 810 -> 624 ms at 78 registers / 37% occupancy).
+__global__ void __launch_bounds__(256, 4) k_project_f64(Grid3 g, const double* __restrict__ srcs,
                                                    const double* __restrict__ det00,
                                                    const double* __restrict__ ustep,
                                                    const double* __restrict__ vstep, int64_t nu, int64_t nv,
