@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(1024, 1) k_bp_boundary(const int64_t* __restri
 //   dt^2 (H(z_k+1) - H(z_k) - 2 f_k (1 - f_k) |r_V_k|^2)
 // (the straddler of the lower boundary contributes (1 - f_k)^2, not 1 - f_k^2); exact while no ray
 // spans a whole voxel height inside one crossing, which the plan checks (bps_mode2_ok).
-template <int GS, bool FLAT, int MAXR, bool MODE2 = false>
+template <int GS, bool FLAT, int MAXR, bool MODE2 = false, bool PAIR = false>
 __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_off,
                                                     const CellEntry* __restrict__ cell_ent,
                                                     const ColumnHeader* __restrict__ cols,
@@ -535,50 +535,66 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
 #endif
         }
         __syncthreads();
-#pragma unroll 2
-        for (int k = 0; k < nch; ++k) {
-            const float4 t0 = s_t0[k], t1 = s_t1[k];
-            const float2 t2 = s_t2[k];
-            const float2* pyc = reinterpret_cast<const float2*>(pref) + s_base[k];
-            asm("mov.b64 %0, %0;" : "+l"(pyc));
-            float P0[G], P1[G];
-            uint32_t bg[G];
+        // PAIR: entries in pairs, the two crossings' dt-weighted boundary values summed before the
+        // neighbour shuffle, H = dt_1 G_1 + dt_2 G_2 and voxel += H(k+1) - H(k), so one shuffle serves
+        // two crossings (the shuffle is a third of the L1 data-pipe work; config 3 104.9 -> 101.0 ms at
+        // GS = 3).  G carries ~1e-7 relative rounding either way; the difference keeps the same
+        // absolute error per crossing.  Without PAIR one entry per shuffle, two entries unrolled.
+        constexpr int EPT = PAIR ? 2 : 1;
+#pragma unroll(PAIR ? 1 : 2)
+        for (int k = 0; k < nch; k += EPT) {
+            float H[G], Cm[MODE2 ? G : 1];
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                // rays entirely below z: rows under W(t_b) above the mid-plane, W(t_a) below
-                const float W = fmaf(zp[g], g < GS ? t0.x : t0.y, t2.x);
-                bg[g] = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));
-                CBCT_DCHECK(s_base[k] + (long long)bg[g] - (long long)s_vuc[k] * nvq >= 0 &&
-                            s_base[k] + (long long)bg[g] - (long long)s_vuc[k] * nvq < nvq);
-                const float2 py = __ldg(pyc + bg[g]);
-                P0[g] = py.x;
-                P1[g] = py.y;
+            for (int e = 0; e < EPT; ++e) {
+                const int ke = k + e;
+                if (e == 1 && ke >= nch) break;
+                const float4 t0 = s_t0[ke], t1 = s_t1[ke];
+                const float2 t2 = s_t2[ke];
+                const float2* pyc = reinterpret_cast<const float2*>(pref) + s_base[ke];
+                asm("mov.b64 %0, %0;" : "+l"(pyc));
+                float P0[G], P1[G];
+                uint32_t bg[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    // rays entirely below z: rows under W(t_b) above the mid-plane, W(t_a) below
+                    const float W = fmaf(zp[g], g < GS ? t0.x : t0.y, t2.x);
+                    bg[g] = (uint32_t)__float_as_int(__fadd_rd(W, 12582912.0f));
+                    CBCT_DCHECK(s_base[ke] + (long long)bg[g] - (long long)s_vuc[ke] * nvq >= 0 &&
+                                s_base[ke] + (long long)bg[g] - (long long)s_vuc[ke] * nvq < nvq);
+                    const float2 py = __ldg(pyc + bg[g]);
+                    P0[g] = py.x;
+                    P1[g] = py.y;
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    // straddle fraction (closed form, k_bp_boundary): s = (W_a - R) kI / z in 1/t,
+                    // f_t = s (1 - eps + eps s); W_a - R = zp sa + (B_a - Bi) - R with every rounding on O(1)
+                    const float R = __int_as_float((int)bg[g]) - 12582911.0f;
+                    const float u = fmaf(zp[g], t1.y, fmaf(zp[g], t0.x, t2.y - R));
+                    const float sv = __saturatef(u * (iz[g] * t0.z));
+                    const float h = fmaf(t1.x, sv, t1.z);
+                    const float f = g < GS ? fmaf(-sv, h, 1.0f) : sv * h;  // below: 1 - f_t ; above: f_t
+                    if (MODE2) {
+                        const float fw = f * P1[g];
+                        const float Gv = fmaf(f, fw, P0[g]);   // P2[V] + f^2 w2
+                        const float c = 2.0f * (fw - f * fw);  // 2 f (1 - f) w2
+                        H[g] = e == 0 ? t0.w * Gv : fmaf(t0.w, Gv, H[g]);
+                        Cm[g] = e == 0 ? t0.w * c : fmaf(t0.w, c, Cm[g]);
+                    } else {
+                        const float Gv = fmaf(f, P1[g], P0[g]);
+                        H[g] = e == 0 ? t0.w * Gv : fmaf(t0.w, Gv, H[g]);
+                    }
+                    if (FLAT) {
+                        const int gi = warp * GS + (g < GS ? g : g - GS);
+                        const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;
+                        acc[g] += (kb == s_fs[ke]) ? t0.w * t1.w : 0.0f;
+                    }
+                }
             }
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                // straddle fraction (closed form, k_bp_boundary): s = (W_a - R) kI / z in 1/t,
-                // f_t = s (1 - eps + eps s); W_a - R = zp sa + (B_a - Bi) - R with every rounding on O(1)
-                const float R = __int_as_float((int)bg[g]) - 12582911.0f;
-                const float u = fmaf(zp[g], t1.y, fmaf(zp[g], t0.x, t2.y - R));
-                const float sv = __saturatef(u * (iz[g] * t0.z));
-                const float h = fmaf(t1.x, sv, t1.z);
-                const float f = g < GS ? fmaf(-sv, h, 1.0f) : sv * h;  // below: 1 - f_t ; above: f_t
-                if (MODE2) {
-                    const float fw = f * P1[g];
-                    const float Gv = fmaf(f, fw, P0[g]);                 // P2[V] + f^2 w2
-                    const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
-                    const float c = 2.0f * (fw - f * fw);                // 2 f (1 - f) w2
-                    acc[g] = fmaf(t0.w, (Gn - Gv) - c, acc[g]);
-                } else {
-                    const float Gv = fmaf(f, P1[g], P0[g]);
-                    const float Gn = __shfl_down_sync(0xffffffffu, Gv, 1);
-                    acc[g] = fmaf(t0.w, Gn - Gv, acc[g]);
-                }
-                if (FLAT) {
-                    const int gi = warp * GS + (g < GS ? g : g - GS);
-                    const int kb = g < GS ? k0 - 31 * (gi + 1) + lane : k0 + 31 * gi + lane;
-                    acc[g] += (kb == s_fs[k]) ? t0.w * t1.w : 0.0f;
-                }
+                const float Hn = __shfl_down_sync(0xffffffffu, H[g], 1);
+                acc[g] += MODE2 ? (Hn - H[g]) - Cm[MODE2 ? g : 0] : Hn - H[g];
             }
         }
     }
@@ -668,12 +684,22 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         const bool sided = !table && (p->bps_ok || mode2_sided);
         // register cap of the sided kernel: 56 for GS = 3 (11 CTAs of 96 threads instead of 10; config 3
         // A^T 107.8 -> 105.7 ms), 64 for GS = 2 (config 5: 56 regs spill, 1379 vs 1418 ms)
+        // entry pairs per shuffle for GS = 3 at 64 registers (config 3: 101.0 ms; 56 registers spill), single
+        // entries at GS = 2 (config 5: pairs 1455 vs 1375 ms)
         static const int regs_env = getenv("CBCT_BP_REGS") ? atoi(getenv("CBCT_BP_REGS")) : 0;
-        const int sided_regs = regs_env ? regs_env : (p->bps_gs == 3 ? 56 : 64);
+        static const int pair_env = getenv("CBCT_BP_PAIR") ? atoi(getenv("CBCT_BP_PAIR")) : -1;
+        const bool pair = pair_env >= 0 ? pair_env != 0 : p->bps_gs == 3;
+        const int sided_regs = regs_env ? regs_env : (p->bps_gs == 3 && !pair ? 56 : 64);
 #define LAUNCH_S1(GS, FL, MR)                                                                                  \
-        if (mode == 2) LAUNCH_S2(GS, FL, MR, true); else LAUNCH_S2(GS, FL, MR, false)
-#define LAUNCH_S2(GS, FL, MR, M2)                                                                              \
-        k_bp_sided<GS, FL, MR, M2><<<grid, p->bps_threads, 0, s>>>(                                           \
+        do {                                                                                                   \
+            if (pair) {                                                                                        \
+                if (mode == 2) LAUNCH_S2(GS, FL, MR, true, true); else LAUNCH_S2(GS, FL, MR, false, true);     \
+            } else {                                                                                           \
+                if (mode == 2) LAUNCH_S2(GS, FL, MR, true, false); else LAUNCH_S2(GS, FL, MR, false, false);   \
+            }                                                                                                  \
+        } while (0)
+#define LAUNCH_S2(GS, FL, MR, M2, PR)                                                                          \
+        k_bp_sided<GS, FL, MR, M2, PR><<<grid, p->bps_threads, 0, s>>>(                                       \
             p->d_cell_off, p->d_cell_ent, p->d_cols, pyb, flatw, vol, col_scale, part, (int)p->nv, (int)p->nz, \
             (int)p->zs, p->lo[2], p->pitch[2], p->det00z, p->pv, (int)p->nx, (int)row0, (int)row1,             \
             p->bp_pad_lo, p->bp_pad_hi, boff, nb, vb, vb > 0, p->bps_k0, p->bps_zero)
