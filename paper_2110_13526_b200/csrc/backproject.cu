@@ -535,19 +535,23 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
 #endif
         }
         __syncthreads();
-        // PAIR: entries in pairs, the two crossings' dt-weighted boundary values summed before the
-        // neighbour shuffle, H = dt_1 G_1 + dt_2 G_2 and voxel += H(k+1) - H(k), so one shuffle serves
-        // two crossings (the shuffle is a third of the L1 data-pipe work; config 3 104.9 -> 101.0 ms at
-        // GS = 3).  G carries ~1e-7 relative rounding either way; the difference keeps the same
-        // absolute error per crossing.  Without PAIR one entry per shuffle, two entries unrolled.
-        constexpr int EPT = PAIR ? 2 : 1;
+        // PAIR: entries in groups of EPT = 4, the crossings' dt-weighted boundary values summed before
+        // the neighbour shuffle, H = sum_e dt_e G_e and voxel += H(k+1) - H(k), so one shuffle serves
+        // four crossings (the shuffle was a third of the L1 data-pipe work; config 3 at GS = 3: one
+        // entry per shuffle 104.9-107.1 ms, two 101.0-102.1, four 96.6-96.8, eight 96.0).  G carries
+        // ~1e-7 relative rounding either way; the difference keeps the same absolute error per
+        // crossing.  Without PAIR one entry per shuffle, two entries unrolled.
+#ifndef CBCT_BP_EPT
+#define CBCT_BP_EPT 4
+#endif
+        constexpr int EPT = PAIR ? CBCT_BP_EPT : 1;
 #pragma unroll(PAIR ? 1 : 2)
         for (int k = 0; k < nch; k += EPT) {
             float H[G], Cm[MODE2 ? G : 1];
 #pragma unroll
             for (int e = 0; e < EPT; ++e) {
                 const int ke = k + e;
-                if (e == 1 && ke >= nch) break;
+                if (e > 0 && ke >= nch) break;
                 const float4 t0 = s_t0[ke], t1 = s_t1[ke];
                 const float2 t2 = s_t2[ke];
                 const float2* pyc = reinterpret_cast<const float2*>(pref) + s_base[ke];

@@ -561,17 +561,22 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         const bool zero = both && g->lo[2] + (double)k0 * g->pitch[2] == 0.0;
         const int64_t nb = (std::min<int64_t>(k0, g->nz) + 30) / 31;
         const int64_t na = (std::max<int64_t>(g->nz - k0, 0) + 30) / 31;
-        // GS in {2, 3} with the least wasted group slots, ties to GS = 2; the sided kernel is used
-        // when at most 10% of its slots are wasted (measured A^T: config 3 GS=3 114 ms vs 128 ms
-        // for k_bp_boundary; config 5 GS=2 1469 vs 1684 ms; config 2 with 2 of 12 slots wasted
-        // 15.1 vs 14.1 ms, so it keeps k_bp_boundary)
+        // GS = 3 (four crossings per shuffle, backproject.cu) when at most 10% of its group slots are
+        // wasted, else GS = 2 under the same rule, else k_bp_boundary.  Measured A^T: config 3 GS=3
+        // 94.9 ms vs 128 for k_bp_boundary; config 5 GS=3 1231 ms vs GS=2 1414-1422 and 1684 for
+        // k_bp_boundary; config 2 (5 + 5 groups, 2 of 12 slots wasted) GS=3 14.6 vs 14.0 ms, so it
+        // keeps k_bp_boundary.
         int best = 0;
-        int64_t best_waste = INT64_MAX, best_slots = 1;
+        int64_t best_waste = 0, best_slots = 1;
         for (int gs : {3, 2}) {
             const int64_t warps = (std::max(nb, na) + gs - 1) / gs;
             if (warps > 32) continue;
             const int64_t waste = warps * gs * 2 - nb - na;
-            if (waste <= best_waste) { best_waste = waste; best = gs; best_slots = warps * gs * 2; }
+            if (best == 0 || (10 * waste <= warps * gs * 2 && 10 * best_waste > best_slots)) {
+                best = gs;
+                best_waste = waste;
+                best_slots = warps * gs * 2;
+            }
         }
         bool use = best > 0 && 10 * best_waste <= best_slots;
         if (const char* e = getenv("CBCT_BP_GS")) { best = atoi(e); use = best > 0; }

@@ -2,7 +2,7 @@
 rule are in profiles/history.md): prefix-projector chunk C = 16 unless two such CTAs no longer fit
 an SM (then 8), boundary groups per warp from {3, 4, 6} by least waste with ties to the larger G,
 view batches of the backprojector growing with the ray-prefix table, and the sided boundary kernel
-(GS in {2, 3} below + above groups per warp) where at most 10% of its group slots are wasted.""" 
+(GS = 3, else 2, below + above groups per warp) where at most 10% of its group slots are wasted."""
 
 import gc
 
@@ -18,7 +18,7 @@ CASES = {
     1: ((64, 90, 128, 96), (16, 3, 1, 0)),     # table-form straddle: k_bp_boundary
     2: ((256, 360, 512, 384), (16, 3, 2, 0)),  # 5 + 5 groups: 2 of 12 sided slots wasted
     3: ((512, 720, 616, 480), (16, 6, 2, 3)),
-    5: ((1024, 1440, 1024, 768), (8, 6, 4, 2)),
+    5: ((1024, 1440, 1024, 768), (8, 6, 4, 3)),
 }
 
 
