@@ -83,3 +83,40 @@ def test_sided_matches_boundary_kernel_closely(monkeypatch):
     b.backproject_internal(y, rb)
     assert float((ra - rb).abs().max() / ra.abs().max()) <= 1e-4
     assert float(torch.linalg.norm(ra - rb) / torch.linalg.norm(ra)) <= 2e-6
+
+
+@pytest.mark.parametrize("gs", [2, 3])
+@pytest.mark.parametrize("zslab", [(300, 64), (100, 64)])
+def test_sided_one_sided_slabs(zslab, gs, monkeypatch):
+    """A z slab entirely above (k0 = 0) or below (k0 = nz + 1) the source plane at config-3 cell
+    sizes: only one side's groups carry voxels, the boundary heights start at z_off != 0 (folded
+    into the per-crossing row offsets), mode 1 and mode 2 against the oracle."""
+    from paper_2110_13526_b200.operator import CbctOperator, ProjectionStack
+
+    monkeypatch.setenv("CBCT_BP_GS", str(gs))
+    vg, tr = baseline_geometry(512, 720, 616, 480, views=(50, 2), zslab=zslab)
+    op = CbctOperator(vg, tr)
+    assert op.info.bp_closed_form == 1 and op.info.bp_sided_gs == gs
+    ref = O.OracleOperator(vg, tr)
+    y = np.random.default_rng(3).standard_normal(op.m).astype(np.float32).astype(np.float64)
+    got, want = op.backproject(ProjectionStack(tr, y)).data, ref.backproject(y)
+    assert max_rel(got, want) <= 1e-4, (zslab, gs, max_rel(got, want))
+    got, want = op.normal_diagonal().data, ref.normal_diagonal()
+    assert max_rel(got, want) <= 1e-4, (zslab, gs, "normal_diagonal", max_rel(got, want))
+
+
+def test_sided_not_used_when_the_source_plane_cuts_a_voxel(monkeypatch):
+    """Both sides present but z = 0 inside a voxel (an off-centre slab): the plan must keep
+    k_bp_boundary even when GS is forced, and the result still matches the oracle."""
+    from paper_2110_13526_b200.operator import CbctOperator, ProjectionStack
+    from paper_2110_13526_b200.geometry import VolumeGeometry
+
+    monkeypatch.setenv("CBCT_BP_GS", "3")
+    vg0, tr = baseline_geometry(512, 720, 616, 480, views=(10, 2))
+    p = vg0.voxel_size[2]
+    vg = VolumeGeometry(vg0.nx, vg0.ny, 40, vg0.voxel_size, (0.0, 0.0, 0.37 * p))
+    op = CbctOperator(vg, tr)
+    assert op.info.bp_closed_form == 1 and op.info.bp_sided_gs == 0
+    y = np.random.default_rng(4).standard_normal(op.m).astype(np.float32).astype(np.float64)
+    got, want = op.backproject(ProjectionStack(tr, y)).data, O.OracleOperator(vg, tr).backproject(y)
+    assert max_rel(got, want) <= 1e-4, max_rel(got, want)
