@@ -369,6 +369,7 @@ __global__ void k_cell_t64(Grid3 g, const int64_t* __restrict__ cell_off, const 
 
 struct Cross {  // one staged crossing (column c, the walk's parameters bounding it)
     double ta, tb;
+    float ia, ib;  // 1 / (t pv) at both ends, fp32: only bound the candidate rows
     int c, pad;
 };
 
@@ -406,14 +407,17 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    const double ipv = 1.0 / pv;
     double z0[ZPT], z1[ZPT], acc[ZPT];
+    float zf0[ZPT], zf1[ZPT];
+    const float c0p = (float)(det00z / pv);
     int iz[ZPT];
 #pragma unroll
     for (int r = 0; r < ZPT; ++r) {
         iz[r] = threadIdx.x + r * blockDim.x;
         z0[r] = g.lo2 + (double)iz[r] * g.p2;
+        zf0[r] = (float)z0[r];
         z1[r] = g.lo2 + (double)(iz[r] + 1) * g.p2;
+        zf1[r] = (float)z1[r];
         acc[r] = 0.0;
     }
     for (int base = 0; base < ne; base += kChunk) {
@@ -421,25 +425,26 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
         __syncthreads();
         for (int k = threadIdx.x; k < nch; k += blockDim.x) {
             const double2 t = cell_t[off + base + k];
-            s_x[k] = Cross{t.x, t.y, cell_ent[off + base + k].vu, 0};
+            s_x[k] = Cross{t.x, t.y, (float)(1.0 / (t.x * pv)), (float)(1.0 / (t.y * pv)), cell_ent[off + base + k].vu, 0};
         }
         __syncthreads();
         for (int k = 0; k < nch; ++k) {
             const Cross x = s_x[k];
             if (!(x.tb > x.ta)) continue;
             const int64_t rb = (int64_t)x.c * nv;
-            const double ia = 1.0 / x.ta, ib = 1.0 / x.tb;
+
 #pragma unroll
             for (int r = 0; r < ZPT; ++r) {
                 if (iz[r] >= nz) continue;
                 // candidate rows from the direct plane parameters: a ray can meet the voxel inside the
                 // crossing only if its row lies in [vmin, vmax]; 1e-6 rows of margin cover the
                 // rounding of these bounds (the exact clip below decides)
-                const double qa0 = z0[r] * ia, qb0 = z0[r] * ib, qa1 = z1[r] * ia, qb1 = z1[r] * ib;
-                const double vmin = (fmin(fmin(qa0, qb0), fmin(qa1, qb1)) - det00z) * ipv;
-                const double vmax = (fmax(fmax(qa0, qb0), fmax(qa1, qb1)) - det00z) * ipv;
-                const int va = max(0, (int)ceil(vmin - 1e-6));
-                const int vb = min(nv - 1, (int)floor(vmax + 1e-6));
+                // (fp32 bounds: ~1e-4 rows of rounding at |v| ~ 1000, covered by 2e-3 rows of margin)
+                const float qa0 = zf0[r] * x.ia, qb0 = zf0[r] * x.ib, qa1 = zf1[r] * x.ia, qb1 = zf1[r] * x.ib;
+                const float vmin = fminf(fminf(qa0, qb0), fminf(qa1, qb1)) - c0p;
+                const float vmax = fmaxf(fmaxf(qa0, qb0), fmaxf(qa1, qb1)) - c0p;
+                const int va = max(0, (int)ceilf(vmin - 2e-3f));
+                const int vb = min(nv - 1, (int)floorf(vmax + 2e-3f));
                 for (int v = va; v <= vb; ++v) {
                     const int64_t ray = rb + v;
                     const int2 is = iz_tab[ray];
