@@ -113,6 +113,22 @@ def test_reconstruct_history_box_and_breakdown(tmp_path, config, phantom_file, p
     np.testing.assert_array_equal(kio.read_volume(out).data, kio.read_volume(phantom_file).data)
 
 
+def test_reconstruct_reference_precision(tmp_path, config, geom, projection_file):
+    """--precision f64 runs the reference-precision path: the written iterate equals the fp64
+    solver's on the same file data, bit for bit."""
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200 import io as kio
+
+    out = tmp_path / "rec64.kvol"
+    assert _main(["--precision", "f64", "reconstruct", config, "--prj", projection_file, "--method", "lsqr",
+                  "--jacobi", "--iters", "6", "--out", str(out)]) == 0
+    vg, tr = geom
+    b = kio.read_projections(projection_file, tr)
+    rep = P.lsqr(P.CbctOperator(vg, tr, precision="f64"), b,
+                 P.SolverConfig(method="lsqr", max_iterations=6, jacobi_precondition=True))
+    np.testing.assert_array_equal(kio.read_volume(out).data, rep.final_x.data)
+
+
 def test_compare_outputs_and_bitwise_reruns(tmp_path, config, phantom_file, projection_file):
     outdir = tmp_path / "cmp"
     assert _main(["compare", config, "--prj", projection_file, "--iters", "3", "--tol", "0.5",
