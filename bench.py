@@ -274,6 +274,9 @@ def run_reference(args, cfg, rank, world):
                    "solver": solver, "precision": "f64", "parallelism": "cpu-openmp"},
         "gups_A": N ** 3 * V / ex["t_A"] / 1e9, "gups_AT": N ** 3 * V / ex["t_AT"] / 1e9,
         "t_A_s": ex["t_A"], "t_AT_s": ex["t_AT"], "t_AT_fixed_s": ex["t_AT_fixed"],
+        # each timed step is a k-view sample (A + A^T), not a full iteration: ms_per_step is the extrapolated
+        # full-iteration time, sample_s the measured per-step wall time
+        "extrapolated": True, "sample_s": t1[0] + t1[1], "sample_views": k,
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port", "sample": sample,
                          "extrapolated": True},
         "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
