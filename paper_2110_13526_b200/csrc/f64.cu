@@ -176,8 +176,9 @@ __global__ void __launch_bounds__(256, 4) k_project_f64(Grid3 g, const double* _
 // seg = (t_end - t) * |r| is the reference's value and only the summation order differs
 // (the reference's own worker count changes that too).
 
-struct RayZ {  // per ray, internal order: the prologue of _traverse (operator.py:60-148)
-    double tmin, tmax, tz0, dtz;
+struct RayZ {  // per ray, internal order: the prologue of _traverse (operator.py:60-148), |r|, entry slab
+    double tmin, tmax, tz0, dtz, len;
+    int iz0, step;  // entry slab and z step (0 for a flat ray)
 };
 
 // |r|, the box clip and the z walk start of every ray (operator.py:60-148).
@@ -195,7 +196,7 @@ __global__ void k_ray_table_f64(Grid3 g, const double* __restrict__ srcs, const 
     const double pz = det00[view * 3 + 2] + (double)u * ustep[view * 3 + 2] + (double)v * vstep[view * 3 + 2];
     const double rx = px - sx, ry = py - sy, rz = pz - sz;
     len[i] = sqrt(rx * rx + ry * ry + rz * rz);
-    RayZ out{0.0, 0.0, 1e300, 1e300};
+    RayZ out{0.0, 0.0, 1e300, 1e300, 0.0, 0, 0};
     int2 iz_st = make_int2(0, 0);
     double tmin = 0.0, tmax = 1.0, t1, t2, tt;
     bool hit = true;
@@ -239,6 +240,9 @@ __global__ void k_ray_table_f64(Grid3 g, const double* __restrict__ srcs, const 
             iz_st.y = stz;
         }
     }
+    out.len = len[i];
+    out.iz0 = iz_st.x;
+    out.step = iz_st.y;
     rz_tab[i] = out;
     iz_tab[i] = iz_st;
 }
@@ -447,10 +451,9 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
                 const int vb = min(nv - 1, (int)floorf(vmax + 2e-3f));
                 for (int v = va; v <= vb; ++v) {
                     const int64_t ray = rb + v;
-                    const int2 is = iz_tab[ray];
-                    const int d = (iz[r] - is.x) * is.y;  // z steps from the entry slab to this slab
-                    if (is.y == 0 ? iz[r] != is.x : d < 0) continue;
-                    const RayZ q = rz_tab[ray];
+                    const RayZ q = rz_tab[ray];  // one 48-byte record per candidate
+                    const int d = (iz[r] - q.iz0) * q.step;  // z steps from the entry slab to this slab
+                    if (q.step == 0 ? iz[r] != q.iz0 : d < 0) continue;
                     double t_in = -1e300, t_out = q.tz0;  // accumulated z planes (tz += dtz)
                     for (int j = 0; j < d; ++j) {
                         t_in = t_out;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
                     const double t0 = fmax(fmax(x.ta, q.tmin), t_in);
                     double t1 = x.tb < t_out ? x.tb : t_out;
                     t1 = t1 < q.tmax ? t1 : q.tmax;
-                    const double seg = (t1 - t0) * len[ray];  // operator.py:158-159
+                    const double seg = (t1 - t0) * q.len;  // operator.py:158-159
                     if (seg > kSegEps) acc[r] += mode == 1 ? seg * y[ray] : seg * seg;  // 162-167
                 }
             }
