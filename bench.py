@@ -329,10 +329,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     run = _new_run(P, op, b, solver, steps + warmup + 1)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    device_loop = solver == "cgls" and run.device_capable()
+    device_loop = hasattr(run, "run_device") and run.device_capable()
     if device_loop:
-        # the CGLS loop runs device-resident (scalars and stop tests on the GPU, no host round trip per
-        # iteration) as replays of one captured CUDA graph of the iteration (solvers.CglsRun.run_device)
+        # CGLS and LSQR run device-resident (scalars and stop tests on the GPU, no host round trip per
+        # iteration) as replays of one captured CUDA graph of the iteration (solvers.*Run.run_device)
+        done0 = run.i if solver == "cgls" else run.updates
         run.run_device(warmup, graph=True)  # warm-up (captures the graph on its first call)
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
@@ -341,9 +342,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             end.record(stream)
             torch.cuda.synchronize()
         run.collect()
-        assert run.i == warmup + steps, "the timed loop must run exactly K iterations"
+        done1 = run.i if solver == "cgls" else run.updates
+        assert done1 - done0 == warmup + steps, "the timed loop must run exactly K iterations"
         launches = steps * run.graph_launches  # libcbct kernels per replayed iteration x replays
-        loop = "device-resident CGLS, CUDA-graph replay per iteration"
+        loop = f"device-resident {sname}, CUDA-graph replay per iteration"
     else:
         # host-driven loop (the reference's scalar recurrences on the host, fp64): each step is one
         # full iteration including its blocking norm reads

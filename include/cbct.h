@@ -171,6 +171,23 @@ int cbct_cgls_volume_update_dev(int64_t n, float* x, float* d, const float* r, c
                                 void* stream);
 int cbct_cgls_proj_update_dev(int64_t n, float* e, const float* p, const double* scalars, double* partials,
                               void* stream);
+/* Device-resident LSQR (solvers.py:361-459): one A, one A^T and two fused vector passes per
+ * iteration.  u and v are kept unnormalised (u = uh / nu, v = vh / nv); the U pass forms
+ * uh <- tmp_m / nv - (alpha / nu) uh with tmp_m = A (scale vh), the V pass first applies the
+ * previous iteration's deferred Givens update (x += a_x w ; w = vh / nv + a_w w) and then forms
+ * vh <- tmp_n / nu - (beta / nv) vh with tmp_n = scale A^T uh, writing sv = scale vh for the next
+ * A when scale != NULL.  Both write fp64 partials of the new vector's squared norm.
+ * cbct_lsqr_scalars: stage 1 after the U pass (beta), stage 2 after the V pass (alpha, the Givens
+ * rotation, the history record phibar at index 24 + iteration, breakdown / tolerance / budget
+ * stops).  cbct_lsqr_flush applies the pending update once the loop has stopped.  Scalar layout:
+ * 0 alpha, 1 beta, 2 rhobar, 3 phibar, 4 nu, 5 nv, 6 a_x, 7 a_w, 8 pending, 9 ||uh||^2,
+ * 10 ||vh||^2, 11 state, 12 iteration, 13 ||b||, 14 tolerance, 15 max updates, 16 final a_x. */
+int cbct_lsqr_u_update(int64_t n, float* uh, const float* tmp_m, const double* scalars, double* partials,
+                       void* stream);
+int cbct_lsqr_v_update(int64_t n, float* x, float* w, float* vh, const float* tmp_n, float* sv, const float* scale,
+                       const double* scalars, double* partials, void* stream);
+int cbct_lsqr_scalars(double* scalars, int stage, void* stream);
+int cbct_lsqr_flush(int64_t n, float* x, const float* w, const float* vh, const double* scalars, void* stream);
 /* Multi-GPU: *out = vals[0] + vals[1] + ... in index order (the per-rank norm partials after an
  * all_gather), the same fp64 additions as the host's rank-ordered sum. */
 int cbct_sum_ranks(const double* vals, int n, double* out, void* stream);

@@ -78,6 +78,10 @@ SIGNATURES = {
     "cbct_cgls_volume_update_dev": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "cbct_cgls_proj_update_dev": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "cbct_sum_ranks": (c_i32, [c_p, c_i32, c_p, c_p]),
+    "cbct_lsqr_u_update": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_lsqr_v_update": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_lsqr_scalars": (c_i32, [c_p, c_i32, c_p]),
+    "cbct_lsqr_flush": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "cbct_cgls_volume_update_p2p": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_i32, c_i64, c_p]),
     "cbct_cgls_proj_update_p2p": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_i32, c_i64, c_p]),
     "cbct_phantom_ref": (c_i32, [c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p]),

@@ -309,6 +309,128 @@ __global__ void k_cgls_proj_dev(int64_t n, float* __restrict__ e, const float* _
     finish(sq, partials);
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-resident LSQR (solvers.py:361-459, Golub-Kahan + Givens) with two fused vector passes
+// per iteration.  u and v are kept unnormalised, u = uh / nu and v = vh / nv, so each
+// normalisation folds into the next pass, and the Givens update of x and w (which needs the
+// new v) is deferred into the next v pass:
+//   U pass:  uh <- tmp_m / nv - (alpha / nu) uh            (= A v - alpha u), ||uh||^2
+//   V pass:  x += a_x w ; w = vh / nv + a_w w               (previous iteration's update)
+//            vh <- tmp_n / nu' - (beta / nv) vh             (= A^T u - beta v), sv = scale vh, ||vh||^2
+// with tmp_m = A (scale vh) and tmp_n = scale A^T uh.  Scalars (fp64, one thread) between them.
+enum : int {
+    kLAlpha = 0, kLBeta = 1, kLRhobar = 2, kLPhibar = 3, kLNu = 4, kLNv = 5, kLAx = 6, kLAw = 7,
+    kLPending = 8, kLU2 = 9, kLV2 = 10, kLState = 11, kLIter = 12, kLNb0 = 13, kLTol = 14, kLMax = 15,
+    kLFinal = 16, kLHist = 24
+};
+
+__global__ void k_lsqr_u(int64_t n, float* __restrict__ uh, const float* __restrict__ tmp_m,
+                         const double* __restrict__ S, double* __restrict__ partials) {
+    if (S[kLState] != 0.0) return;
+    const float c1 = (float)(1.0 / S[kLNv]), c2 = (float)(S[kLAlpha] / S[kLNu]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float v = fmaf(tmp_m[i], c1, -c2 * uh[i]);
+        uh[i] = v;
+        sq += (double)v * v;
+    }
+    finish(sq, partials);
+}
+
+__global__ void k_lsqr_v(int64_t n, float* __restrict__ x, float* __restrict__ w, float* __restrict__ vh,
+                         const float* __restrict__ tmp_n, float* __restrict__ sv, const float* __restrict__ scale,
+                         const double* __restrict__ S, double* __restrict__ partials) {
+    if (S[kLState] != 0.0) return;
+    const bool pend = S[kLPending] != 0.0;
+    const float ax = (float)S[kLAx], aw = (float)S[kLAw], inv_nv = (float)(1.0 / S[kLNv]);
+    const float c1 = (float)(1.0 / S[kLNu]), c2 = (float)(S[kLBeta] / S[kLNv]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float vo = vh[i];
+        if (pend) {
+            const float wv = w[i];
+            x[i] = fmaf(ax, wv, x[i]);
+            w[i] = fmaf(aw, wv, vo * inv_nv);
+        }
+        const float v = fmaf(tmp_n[i], c1, -c2 * vo);
+        vh[i] = v;
+        if (sv) sv[i] = scale[i] * v;
+        sq += (double)v * v;
+    }
+    finish(sq, partials);
+}
+
+// x += a_x w (the deferred update of the last iteration); after a zero-beta breakdown also the
+// final Givens step with the updated w, x += a_final (v + a_w w)
+__global__ void k_lsqr_flush(int64_t n, float* __restrict__ x, const float* __restrict__ w,
+                             const float* __restrict__ vh, const double* __restrict__ S) {
+    if (S[kLPending] == 0.0) return;
+    const float ax = (float)S[kLAx], aw = (float)S[kLAw], af = (float)S[kLFinal], inv_nv = (float)(1.0 / S[kLNv]);
+    const bool fin = S[kLFinal] != 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const float wv = w[i];
+        float xv = fmaf(ax, wv, x[i]);
+        if (fin) xv = fmaf(af, fmaf(aw, wv, vh[i] * inv_nv), xv);
+        x[i] = xv;
+    }
+}
+
+// stage 1, after the U pass: beta, nu.  stage 2, after the V pass: alpha, nv, the Givens
+// rotation (solvers.py:443-452), the deferred update's coefficients, the history record and the
+// stop tests.  A zero beta or alpha (breakdown) stops the loop with the state the reference
+// leaves: the final x update is pending (a_x) and applied by k_lsqr_flush.
+__global__ void k_lsqr_scalars(double* __restrict__ S, int stage) {
+    if (S[kLState] != 0.0) return;
+    if (stage == 1) {
+        const double beta = sqrt(S[kLU2]);
+        S[kLBeta] = beta;
+        S[kLNu] = beta;  // u = uh / beta from here on (the V pass divides A^T uh by it)
+        if (beta == 0.0) {  // solvers.py:432-452 with beta = 0: alpha kept, Givens, then break
+            const double rhobar = S[kLRhobar];
+            const double rho = hypot(rhobar, 0.0);
+            const double c = rhobar / rho;
+            const double phi = c * S[kLPhibar];
+            S[kLPhibar] = 0.0;
+            S[kLFinal] = phi / rho;  // applied by k_lsqr_flush after the pending update (pending if it > 0)
+            if (S[kLIter] == 0.0) {  // no earlier update pending: the final step alone
+                S[kLAx] = 0.0;
+                S[kLAw] = 0.0;
+                S[kLPending] = 1.0;
+            }
+            const double it = S[kLIter];
+            S[kLHist + (int)it] = 0.0;
+            S[kLIter] = it + 1.0;
+            S[kLState] = 1.0;
+            return;
+        }
+        return;
+    }
+    const double alpha = sqrt(S[kLV2]), beta = S[kLBeta];
+    const double rho = hypot(S[kLRhobar], beta);
+    const double c = S[kLRhobar] / rho, s = beta / rho;
+    const double theta = s * alpha;
+    S[kLRhobar] = -c * alpha;
+    const double phi = c * S[kLPhibar];
+    S[kLPhibar] = s * S[kLPhibar];
+    S[kLAx] = phi / rho;
+    S[kLAw] = -(theta / rho);
+    S[kLPending] = 1.0;
+    S[kLAlpha] = alpha;
+    S[kLNv] = alpha;
+    const double it = S[kLIter];
+    S[kLHist + (int)it] = S[kLPhibar];
+    S[kLIter] = it + 1.0;
+    const double nb0 = S[kLNb0];
+    const double rel = nb0 > 0.0 ? S[kLPhibar] / nb0 : 0.0;
+    if (alpha == 0.0) S[kLState] = 1.0;                          // breakdown (v stays 0)
+    else if (S[kLTol] > 0.0 && rel <= S[kLTol]) S[kLState] = 2.0;  // converged
+    else if (it + 1.0 >= S[kLMax]) S[kLState] = 3.0;               // budget (max_iterations + 1 updates)
+}
+
 }  // namespace
 
 extern "C" int cbct_vec_blocks(int64_t n) { return vec_blocks(n); }
@@ -461,6 +583,42 @@ extern "C" int cbct_cgls_proj_update_p2p(int64_t n, const float* e_own, const fl
     const int use4 = aligned16(e_own) && aligned16(p) && (offset & 3) == 0;
     k_cgls_proj_dev_p2p<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, e_own, p, scalars, partials, peers,
                                                                               npeers, offset, use4);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_lsqr_u_update(int64_t n, float* uh, const float* tmp_m, const double* scalars,
+                                  double* partials, void* stream) {
+    if (!uh || !tmp_m || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_lsqr_u_update: null argument");
+    k_lsqr_u<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, uh, tmp_m, scalars, partials);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_lsqr_v_update(int64_t n, float* x, float* w, float* vh, const float* tmp_n, float* sv,
+                                  const float* scale, const double* scalars, double* partials, void* stream) {
+    if (!x || !w || !vh || !tmp_n || !scalars || (sv && !scale))
+        return cbct_fail(CBCT_E_ARG, "cbct_lsqr_v_update: bad argument");
+    k_lsqr_v<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, w, vh, tmp_n, sv, scale, scalars, partials);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_lsqr_flush(int64_t n, float* x, const float* w, const float* vh, const double* scalars,
+                               void* stream) {
+    if (!x || !w || !vh || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_lsqr_flush: null argument");
+    k_lsqr_flush<<<vec_blocks(n), kThreads, 0, (cudaStream_t)stream>>>(n, x, w, vh, scalars);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_lsqr_scalars(double* scalars, int stage, void* stream) {
+    if (!scalars || stage < 1 || stage > 2) return cbct_fail(CBCT_E_ARG, "cbct_lsqr_scalars: bad argument");
+    k_lsqr_scalars<<<1, 1, 0, (cudaStream_t)stream>>>(scalars, stage);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();
     return 0;

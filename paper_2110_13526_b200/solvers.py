@@ -685,14 +685,101 @@ class LsqrRun:
 
     def report(self) -> SolverReport:
         op = self.op
+        if getattr(self, "_S", None) is not None:  # device-resident iterations: apply the pending update
+            call("cbct_lsqr_flush", self.x.numel(), _p(self.x), _p(self.w), _p(self.v), _p(self._S), self.dev.s())
+            self._S = None
         return SolverReport(_final_volume(op, self.chain.x_of(self.x), self.b.data), len(self.history) - 1,
                             self.phibar, self.history, getattr(op, "workers", 1), self.breakdown)
 
+    # ------------------------------------------------- device-resident iterations --
+    def device_capable(self) -> bool:
+        """The fp32 fused chain, plain or Jacobi-preconditioned (no Tikhonov stacking, no true-discrepancy
+        monitoring), runs with every scalar on the device (``run_device``)."""
+        c = self.chain
+        inner = c.inner if isinstance(c, _JacobiChain) else c
+        return (type(c) in (_Chain, _JacobiChain) and type(inner) is _Chain and inner._fused and
+                self.cfg.true_discrepancy_every <= 0 and not self.dev.f64 and not self.done)
+
+    def _device_state(self):
+        """Scalar array of include/cbct.h cbct_lsqr_scalars, loaded from the host state after the
+        pre-loop (u and v normalised: nu = nv = 1; w = v, no update pending)."""
+        if getattr(self, "_S", None) is None:
+            K = self.cfg.max_iterations
+            self._S = torch.zeros(24 + K + 2, dtype=torch.float64, device=self.dev.device)
+            host = torch.tensor([self.alpha, 0.0, self.rhobar, self.phibar, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0,
+                                 float(self.updates), self.nb0, float(self.cfg.rel_discrepancy_tol), float(K + 1),
+                                 0.0], dtype=torch.float64)
+            self._S[:17].copy_(host)
+            self._jac = self.chain.scale if isinstance(self.chain, _JacobiChain) else None
+            self._sv = torch.empty_like(self.v) if self._jac is not None else None
+            if self._jac is not None:
+                self.dev.mul(self.v, self._jac, self._sv)
+            self._inner = self.chain.inner if self._jac is not None else self.chain
+        return self._S
+
+    def _device_iteration(self, S):
+        op, dev, st = self.op, self.dev, self.dev.s
+        inner = self._inner
+        op.project_internal(self._sv if self._jac is not None else self.v, self.tmp_m)
+        call("cbct_lsqr_u_update", self.u.numel(), _p(self.u), _p(self.tmp_m), _p(S), _p(dev.partials), st())
+        op.reduce_to(dev.nblocks(self.u.numel()), S[9:10])
+        call("cbct_lsqr_scalars", _p(S), 1, st())
+        op.backproject_internal(self.u, self.tmp_n, scratch=inner._scratch(), col_scale=self._jac)
+        call("cbct_lsqr_v_update", self.v.numel(), _p(self.x), _p(self.w), _p(self.v), _p(self.tmp_n),
+             _p(self._sv), _p(self._jac), _p(S), _p(dev.partials), st())
+        op.reduce_to(dev.nblocks(self.v.numel()), S[10:11])
+        call("cbct_lsqr_scalars", _p(S), 2, st())
+
+    def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
+        """Up to k LSQR iterations with the scalars on the device: one A, one A^T and two fused
+        vector passes each (include/cbct.h cbct_lsqr_*), no host round trip inside; ``graph`` replays
+        one captured CUDA graph of the iteration.  Once used, the run stays on the device (its
+        vectors are kept unnormalised); ``report`` applies the pending update."""
+        if self.done or k <= 0:
+            return
+        S = self._device_state()
+        self._i0 = self.updates
+        if graph:
+            if getattr(self, "_graph", None) is None:
+                from ._lib import lib
+
+                g = torch.cuda.CUDAGraph()
+                n0 = lib().cbct_launch_count()
+                with torch.cuda.graph(g):
+                    self._device_iteration(S)
+                self.graph_launches = lib().cbct_launch_count() - n0
+                self._graph = g
+            for _ in range(k):
+                self._graph.replay()
+        else:
+            for _ in range(k):
+                self._device_iteration(S)
+        if collect:
+            self.collect()
+
+    def collect(self) -> None:
+        h = self._S.cpu().numpy()
+        it = int(h[12])
+        now = time.perf_counter() - self.t0
+        for j in range(self._i0, it):
+            self.history.append(ConvergenceRecord(j, now, self.rel(float(h[24 + j])), None))
+        self.updates = it
+        self.phibar = float(h[3])
+        if h[11] != 0.0:
+            self.done = True
+            self.breakdown = h[11] == 1.0
+
 
 def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
-    """LSQR (solvers.py:361-459): Golub-Kahan bidiagonalisation + Givens."""
+    """LSQR (solvers.py:361-459): Golub-Kahan bidiagonalisation + Givens.  The fp32 fused chain runs
+    device-resident (two fused vector passes per iteration, no host round trip); the fp64 path,
+    wrapped operators, Tikhonov stacking and true-discrepancy monitoring use the host loop."""
     _check_inputs(op, b, cfg, "lsqr")
     run = LsqrRun(op, b, cfg)
+    if run.device_capable():
+        while run.should_continue():
+            run.run_device(min(_DEVICE_BATCH, cfg.max_iterations + 1 - run.updates))
+        return run.report()
     while run.should_continue():
         run.step()
     return run.report()

@@ -195,9 +195,14 @@ def test_sharded_mode2_and_col_scale_assemble_to_full(world):
     assert torch.equal(torch.cat(r_parts)[: full.vol_elems], r_full)
 
 
-def test_nccl_world1_lsqr_and_psirt_drivers_match_single_gpu():
+def test_nccl_world1_lsqr_and_psirt_drivers_match_single_gpu(monkeypatch):
     """dist_lsqr (Jacobi) and dist_psirt over NCCL at world size 1 run the same vector kernels and
-    reductions as solvers.lsqr / solvers.psirt: identical histories and iterates."""
+    reductions as the single-GPU host loops of solvers.lsqr / solvers.psirt: identical histories
+    and iterates (the single-GPU fp32 LSQR otherwise runs device-resident, in another rounding
+    order -- compared in test_solvers_gpu.py)."""
+    import paper_2110_13526_b200.solvers as S
+
+    monkeypatch.setattr(S.LsqrRun, "device_capable", lambda self: False)
     import torch.distributed as dist
 
     import paper_2110_13526_b200 as P

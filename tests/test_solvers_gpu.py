@@ -421,3 +421,37 @@ def test_dense_oracle_equivalence_f64():
         assert rel_l2(rep.final_x.data, x_ls) <= 1e-6, m
         rep = S.solve(op, b, S.SolverConfig(method=m, max_iterations=600, tikhonov_lambda=1.0))
         assert rel_l2(rep.final_x.data, closed) <= 1e-6, m
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_device_resident_lsqr_matches_the_host_loop(jacobi, monkeypatch):
+    """The fp32 fused chain runs LSQR device-resident: u and v kept unnormalised, two fused vector
+    passes per iteration, the Givens update deferred into the next v pass (include/cbct.h
+    cbct_lsqr_*).  Same recurrences as the host loop (solvers.py:427-458) in another rounding
+    order: histories agree to 2e-5 and iterates within the north-star 1e-3, the tolerance stop lands
+    on the same record, and a graph-replayed run equals the launched one bitwise.  BASELINE config 1
+    (64^3, 90 views): well conditioned, so rounding-order differences stay at fp32 level (the desk
+    problem amplifies them ~1e4 past iteration 10)."""
+    P, S = _mods()
+    from _helpers import baseline_geometry
+
+    vg, tr = baseline_geometry(64, 90, 128, 96)
+    op = P.CbctOperator(vg, tr)
+    b = P.ProjectionStack(tr, O.OracleOperator(vg, tr).project(O.shepp_logan_phantom(vg)))
+    for cfg in (S.SolverConfig(method="lsqr", max_iterations=8, jacobi_precondition=jacobi),
+                S.SolverConfig(method="lsqr", max_iterations=40, jacobi_precondition=jacobi, rel_discrepancy_tol=0.05)):
+        dev = S.lsqr(op, b, cfg)
+        assert S.LsqrRun(op, b, cfg).device_capable()
+        monkeypatch.setattr(S.LsqrRun, "device_capable", lambda self: False)
+        host = S.lsqr(op, b, cfg)
+        monkeypatch.undo()
+        assert dev.iterations == host.iterations and dev.breakdown == host.breakdown
+        np.testing.assert_allclose(_hist(dev), _hist(host), rtol=2e-5)
+        # x carries the ill-conditioned directions the residual does not see (measured <= 2.2e-4)
+        assert rel_l2(dev.final_x.data, host.final_x.data) <= 1e-3
+    run = S.LsqrRun(op, b, S.SolverConfig(method="lsqr", max_iterations=6, jacobi_precondition=jacobi))
+    run.run_device(7, graph=True)
+    ref = S.LsqrRun(op, b, S.SolverConfig(method="lsqr", max_iterations=6, jacobi_precondition=jacobi))
+    ref.run_device(7)
+    assert [h.rel_discrepancy for h in run.history] == [h.rel_discrepancy for h in ref.history]
+    assert torch.equal(run.x, ref.x) and torch.equal(run.w, ref.w)
