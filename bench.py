@@ -333,7 +333,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if device_loop:
         # CGLS and LSQR run device-resident (scalars and stop tests on the GPU, no host round trip per
         # iteration) as replays of one captured CUDA graph of the iteration (solvers.*Run.run_device)
-        done0 = run.i if solver == "cgls" else run.updates
+        done0 = run.updates if solver == "lsqr-jacobi" else run.i
         run.run_device(warmup, graph=True)  # warm-up (captures the graph on its first call)
         torch.cuda.synchronize()
         with ClockSampler(local_rank) as clk:
@@ -342,7 +342,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             end.record(stream)
             torch.cuda.synchronize()
         run.collect()
-        done1 = run.i if solver == "cgls" else run.updates
+        done1 = run.updates if solver == "lsqr-jacobi" else run.i
         assert done1 - done0 == warmup + steps, "the timed loop must run exactly K iterations"
         launches = steps * run.graph_launches  # libcbct kernels per replayed iteration x replays
         loop = f"device-resident {sname}, CUDA-graph replay per iteration"

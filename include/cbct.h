@@ -188,6 +188,16 @@ int cbct_lsqr_v_update(int64_t n, float* x, float* w, float* vh, const float* tm
                        const double* scalars, double* partials, void* stream);
 int cbct_lsqr_scalars(double* scalars, int stage, void* stream);
 int cbct_lsqr_flush(int64_t n, float* x, const float* w, const float* vh, const double* scalars, void* stream);
+/* Device-resident SIRT / PSIRT (solvers.py:505-569).  Volume pass: x += step upd (or step_vec * upd,
+ * SIRT), then clip to [lo, hi] on the voxels if clip.  Projection pass: r = b - p, w = r * inv_row,
+ * fp64 partials of r^2.  cbct_psirt_scalars: history record sqrt(||r||^2) / ||b|| at index
+ * 8 + iteration, tolerance and budget stops.  Scalar layout: 0 ||r||^2, 1 state, 2 iteration,
+ * 3 ||b||, 4 tolerance, 5 max iterations. */
+int cbct_psirt_volume_update(const cbct_plan* plan, float* x, const float* upd, const float* step_vec, float step,
+                             int clip, float lo, float hi, const double* scalars, void* stream);
+int cbct_psirt_proj_update(int64_t m, float* r, float* w, const float* b, const float* p, const float* inv_row,
+                           const double* scalars, double* partials, void* stream);
+int cbct_psirt_scalars(double* scalars, void* stream);
 /* Multi-GPU: *out = vals[0] + vals[1] + ... in index order (the per-rank norm partials after an
  * all_gather), the same fp64 additions as the host's rank-ordered sum. */
 int cbct_sum_ranks(const double* vals, int n, double* out, void* stream);

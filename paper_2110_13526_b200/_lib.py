@@ -82,6 +82,9 @@ SIGNATURES = {
     "cbct_lsqr_v_update": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
     "cbct_lsqr_scalars": (c_i32, [c_p, c_i32, c_p]),
     "cbct_lsqr_flush": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_psirt_volume_update": (c_i32, [c_p, c_p, c_p, c_p, c_f32, c_i32, c_f32, c_f32, c_p, c_p]),
+    "cbct_psirt_proj_update": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "cbct_psirt_scalars": (c_i32, [c_p, c_p]),
     "cbct_cgls_volume_update_p2p": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_i32, c_i64, c_p]),
     "cbct_cgls_proj_update_p2p": (c_i32, [c_i64, c_p, c_p, c_p, c_p, c_p, c_i32, c_i64, c_p]),
     "cbct_phantom_ref": (c_i32, [c_i64, c_i64, c_i64, c_p, c_i32, c_p, c_p]),

@@ -431,6 +431,57 @@ __global__ void k_lsqr_scalars(double* __restrict__ S, int stage) {
     else if (it + 1.0 >= S[kLMax]) S[kLState] = 3.0;               // budget (max_iterations + 1 updates)
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-resident SIRT / PSIRT (solvers.py:505-569): per iteration A^T w, one fused volume pass
+// (x += step upd, or step_vec * upd for SIRT, then the box clip on the voxels), A x, one fused
+// projection pass (r = b - A x, w = r / row sums for the next A^T, ||r||^2) and a one-thread
+// scalar stage (history, tolerance and budget stops).  Same values as the host loop's
+// mul / axpby / clip / sub kernels.
+enum : int { kPR2 = 0, kPState = 1, kPIter = 2, kPNb0 = 3, kPTol = 4, kPMax = 5, kPHist = 8 };
+
+__global__ void k_psirt_volume(int64_t n, int64_t zs, int64_t nz, float* __restrict__ x,
+                               const float* __restrict__ upd, const float* __restrict__ step_vec, float step,
+                               int clip, float lo, float hi, const double* __restrict__ S) {
+    if (S[kPState] != 0.0) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        // SIRT: the product rounded on its own (__fmul_rn: no contraction), as the host loop's mul + axpby
+        float xv = step_vec ? __fadd_rn(__fmul_rn(upd[i], step_vec[i]), x[i]) : fmaf(step, upd[i], 1.0f * x[i]);
+        if (clip) {
+            const int64_t k = i % zs;
+            if (k >= CBCT_ZPAD && k < CBCT_ZPAD + nz) xv = fminf(fmaxf(xv, lo), hi);
+        }
+        x[i] = xv;
+    }
+}
+
+__global__ void k_psirt_proj(int64_t m, float* __restrict__ r, float* __restrict__ w, const float* __restrict__ b,
+                             const float* __restrict__ p, const float* __restrict__ inv_row,
+                             const double* __restrict__ S, double* __restrict__ partials) {
+    if (S[kPState] != 0.0) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double sq = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
+        const float rv = b[i] - p[i];
+        r[i] = rv;
+        w[i] = rv * inv_row[i];
+        sq += (double)rv * rv;
+    }
+    finish(sq, partials);
+}
+
+__global__ void k_psirt_scalars(double* __restrict__ S) {
+    if (S[kPState] != 0.0) return;
+    const double nb0 = S[kPNb0];
+    const double e = nb0 > 0.0 ? sqrt(S[kPR2]) / nb0 : 0.0;
+    const double it = S[kPIter] + 1.0;
+    S[kPIter] = it;
+    S[kPHist + (int)it] = e;
+    if (S[kPTol] > 0.0 && e <= S[kPTol]) S[kPState] = 2.0;
+    else if (it >= S[kPMax]) S[kPState] = 3.0;
+}
+
 }  // namespace
 
 extern "C" int cbct_vec_blocks(int64_t n) { return vec_blocks(n); }
@@ -619,6 +670,34 @@ extern "C" int cbct_lsqr_flush(int64_t n, float* x, const float* w, const float*
 extern "C" int cbct_lsqr_scalars(double* scalars, int stage, void* stream) {
     if (!scalars || stage < 1 || stage > 2) return cbct_fail(CBCT_E_ARG, "cbct_lsqr_scalars: bad argument");
     k_lsqr_scalars<<<1, 1, 0, (cudaStream_t)stream>>>(scalars, stage);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_psirt_volume_update(const cbct_plan* p, float* x, const float* upd, const float* step_vec,
+                                        float step, int clip, float lo, float hi, const double* scalars,
+                                        void* stream) {
+    if (!p || !x || !upd || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_psirt_volume_update: null argument");
+    k_psirt_volume<<<vec_blocks(p->vol_elems), kThreads, 0, (cudaStream_t)stream>>>(
+        p->vol_elems, p->zs, p->nz, x, upd, step_vec, step, clip, lo, hi, scalars);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_psirt_proj_update(int64_t m, float* r, float* w, const float* b, const float* p,
+                                      const float* inv_row, const double* scalars, double* partials, void* stream) {
+    if (!r || !w || !b || !p || !inv_row || !scalars) return cbct_fail(CBCT_E_ARG, "cbct_psirt_proj_update: null argument");
+    k_psirt_proj<<<vec_blocks(m), kThreads, 0, (cudaStream_t)stream>>>(m, r, w, b, p, inv_row, scalars, partials);
+    CBCT_CHECK(cudaGetLastError());
+    cbct_count_launch();
+    return 0;
+}
+
+extern "C" int cbct_psirt_scalars(double* scalars, void* stream) {
+    if (!scalars) return cbct_fail(CBCT_E_ARG, "cbct_psirt_scalars: null argument");
+    k_psirt_scalars<<<1, 1, 0, (cudaStream_t)stream>>>(scalars);
     CBCT_CHECK(cudaGetLastError());
     cbct_count_launch();
     return 0;

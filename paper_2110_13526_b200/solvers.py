@@ -895,11 +895,80 @@ class ClassicalRun:
         return SolverReport(_final_volume(op, self.x, self.b.data), self.i, self.e * self.nb0, self.history,
                             getattr(op, "workers", 1), False)
 
+    # ------------------------------------------------- device-resident iterations --
+    def device_capable(self) -> bool:
+        """The fp32 fused operator without true-discrepancy monitoring runs with the stop tests on the
+        device (``run_device``): A^T, one fused volume pass, A, one fused projection pass; bitwise the
+        host loop's values (same kernels' arithmetic and reduction grids)."""
+        return self.chain._fused and not self.dev.f64 and self.cfg.true_discrepancy_every <= 0
+
+    def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
+        if k <= 0 or not self.should_continue():
+            return
+        dev, op = self.dev, self.op
+        if getattr(self, "_S", None) is None:
+            self._S = torch.zeros(8 + self.cfg.max_iterations + 2, dtype=torch.float64, device=dev.device)
+            self._S[:6].copy_(torch.tensor([0.0, 0.0, float(self.i), self.nb0, float(self.cfg.rel_discrepancy_tol),
+                                            float(self.cfg.max_iterations)], dtype=torch.float64))
+            dev.mul(self.resid, self.inv_row, self.weighted)
+            self._inv_row32 = self.inv_row.to(dev.dtype).contiguous()
+            self._step_vec = self.step_vec.contiguous() if self.step_vec is not None else None
+        S = self._S
+        self._i0 = self.i
+        clip = self.lo is not None
+        lo = float(self.lo) if clip else 0.0
+        hi = float(self.hi) if clip else 0.0
+
+        def iteration():
+            st = dev.s()
+            op.backproject_internal(self.weighted, self.upd, scratch=self.chain._scratch())
+            call("cbct_psirt_volume_update", self.dev.plan, _p(self.x), _p(self.upd), _p(self._step_vec),
+                 ctypes.c_float(self.step_size if self.step_size is not None else 0.0), int(clip),
+                 ctypes.c_float(lo), ctypes.c_float(hi), _p(S), st)
+            op.project_internal(self.x, self.tmp_p)
+            call("cbct_psirt_proj_update", self.resid.numel(), _p(self.resid), _p(self.weighted), _p(self.b_int),
+                 _p(self.tmp_p), _p(self._inv_row32), _p(S), _p(dev.partials), st)
+            op.reduce_to(dev.nblocks(self.resid.numel()), S[0:1])
+            call("cbct_psirt_scalars", _p(S), st)
+
+        if not hasattr(self, "tmp_p"):
+            self.tmp_p = torch.empty_like(self.resid)
+        if graph:
+            if getattr(self, "_graph", None) is None:
+                from ._lib import lib
+
+                g = torch.cuda.CUDAGraph()
+                n0 = lib().cbct_launch_count()
+                with torch.cuda.graph(g):
+                    iteration()
+                self.graph_launches = lib().cbct_launch_count() - n0
+                self._graph = g
+            for _ in range(k):
+                self._graph.replay()
+        else:
+            for _ in range(k):
+                iteration()
+        if collect:
+            self.collect()
+
+    def collect(self) -> None:
+        h = self._S.cpu().numpy()
+        it = int(h[2])
+        now = time.perf_counter() - self.t0
+        for j in range(self._i0 + 1, it + 1):
+            self.e = float(h[8 + j])
+            self.history.append(ConvergenceRecord(j, now, self.e, None))
+        self.i = it
+
 
 def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solvers.py:505-569
     _check_inputs(op, b, cfg, method)
     run = ClassicalRun(op, b, cfg, method)
     err = cfg.rel_discrepancy_tol
+    if run.device_capable():
+        while run.should_continue():
+            run.run_device(min(_DEVICE_BATCH, cfg.max_iterations - run.i))
+        return run.report()
     while run.should_continue():
         run.step()
         if err > 0.0 and run.e <= err:

@@ -455,3 +455,34 @@ def test_device_resident_lsqr_matches_the_host_loop(jacobi, monkeypatch):
     ref.run_device(7)
     assert [h.rel_discrepancy for h in run.history] == [h.rel_discrepancy for h in ref.history]
     assert torch.equal(run.x, ref.x) and torch.equal(run.w, ref.w)
+
+
+@pytest.mark.parametrize("method,box", [("psirt", None), ("psirt", (0.0, 0.9)), ("sirt", None)])
+def test_device_resident_psirt_sirt_are_bitwise_the_host_loop(method, box, monkeypatch):
+    """SIRT / PSIRT device-resident (A^T, one fused volume pass with the box clip, A, one fused
+    projection pass computing r, R^-1 r and ||r||^2, one-thread stop tests: include/cbct.h
+    cbct_psirt_*) run the host loop's arithmetic on the same reduction grids: bitwise equal
+    histories and iterates, with and without the tolerance stop, graph replay included."""
+    P, S = _mods()
+    from _helpers import baseline_geometry
+
+    vg, tr = baseline_geometry(64, 90, 128, 96)
+    op = P.CbctOperator(vg, tr)
+    b = P.ProjectionStack(tr, O.OracleOperator(vg, tr).project(O.shepp_logan_phantom(vg)))
+    for tol in (0.0, 0.2):
+        cfg = S.SolverConfig(method=method, max_iterations=9, box_bounds=box, rel_discrepancy_tol=tol)
+        dev = S.solve(op, b, cfg)
+        assert S.ClassicalRun(op, b, cfg, method).device_capable()
+        monkeypatch.setattr(S.ClassicalRun, "device_capable", lambda self: False)
+        host = S.solve(op, b, cfg)
+        monkeypatch.undo()
+        assert dev.iterations == host.iterations
+        assert _hist(dev).tolist() == _hist(host).tolist()
+        np.testing.assert_array_equal(dev.final_x.data, host.final_x.data)
+    cfg = S.SolverConfig(method=method, max_iterations=5, box_bounds=box)
+    g = S.ClassicalRun(op, b, cfg, method)
+    g.run_device(5, graph=True)
+    ref = S.ClassicalRun(op, b, cfg, method)
+    ref.run_device(5)
+    assert [h.rel_discrepancy for h in g.history] == [h.rel_discrepancy for h in ref.history]
+    assert torch.equal(g.x, ref.x)
