@@ -631,6 +631,7 @@ __global__ void __maxnreg__(MAXR) k_bp_sided(const int64_t* __restrict__ cell_of
 extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, float* vol, int64_t row0, int64_t row1,
                                      int mode, float* scratch, const float* col_scale, double* partials,
                                      void* stream) {
+    CbctRange range(mode == 2 ? "cbct_normal_diagonal" : "cbct_backproject");
     if (p && (row0 < 0 || row1 > p->ny || row0 >= row1))
         return cbct_fail(CBCT_E_ARG, "cbct_backproject: bad row range");
     if (!p || !vol || !scratch) return cbct_fail(CBCT_E_ARG, "cbct_backproject: null argument");

@@ -14,9 +14,20 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/cbct.h"
 
-#define CBCT_CHECK(expr)                                       \
+// NVTX range over an entry point (header-only NVTX3: a no-op unless a profiler injects itself),
+// so nsys / ncu --nvtx timelines show which operator call a kernel belongs to.
+struct CbctRange {
+    explicit CbctRange(const char* name) { nvtxRangePushA(name); }
+    ~CbctRange() { nvtxRangePop(); }
+    CbctRange(const CbctRange&) = delete;
+    CbctRange& operator=(const CbctRange&) = delete;
+};
+
+#define CBCT_CHECK(expr)                                      \
     do {                                                       \
         cudaError_t _e = (expr);                               \
         if (_e != cudaSuccess) return cbct_fail_cuda(_e, #expr); \

@@ -672,6 +672,7 @@ extern "C" int cbct_f64_vec_blocks(int64_t n) { return vblocks(n); }
 
 extern "C" int cbct_project_f64(const cbct_plan* p, const double* vol, double* proj, double* partials,
                                 void* stream) {
+    CbctRange range("cbct_project_f64");
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project_f64: null argument");
     const int blocks = cbct_f64_proj_blocks(p);
     k_project_f64<<<blocks, 256, 0, (cudaStream_t)stream>>>(grid3(p), p->d_srcs, p->d_det00, p->d_ustep, p->d_vstep,
@@ -688,6 +689,7 @@ extern "C" int cbct_f64_proj_blocks(const cbct_plan* p) {
 
 extern "C" int cbct_backproject_f64(const cbct_plan* p, const double* proj, double* vol, int mode,
                                     const double* col_scale, double* partials, void* stream) {
+    CbctRange range(mode == 2 ? "cbct_normal_diagonal_f64" : "cbct_backproject_f64");
     if (!p || !vol) return cbct_fail(CBCT_E_ARG, "cbct_backproject_f64: null argument");
     if (mode != 1 && mode != 2) return cbct_fail(CBCT_E_ARG, "cbct_backproject_f64: mode must be 1 or 2");
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject_f64: mode 1 needs projections");

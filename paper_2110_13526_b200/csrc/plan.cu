@@ -289,6 +289,7 @@ extern "C" int cbct_plan_destroy(cbct_plan* p) {
 }
 
 extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* stream_) {
+    CbctRange range("cbct_plan_create");
     if (!out || !g || !g->srcs || !g->det00 || !g->ustep || !g->vstep)
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: null argument");
     *out = nullptr;

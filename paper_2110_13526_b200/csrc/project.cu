@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(544) k_project_q(const ColumnHeader* __restric
 
 extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* proj, int64_t view0, int64_t view1,
                                   double* partials, void* stream) {
+    CbctRange range("cbct_project");
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project: null argument");
     if (view0 < 0 || view1 > p->V || view0 >= view1) return cbct_fail(CBCT_E_ARG, "cbct_project: bad view range");
     cudaStream_t s = (cudaStream_t)stream;

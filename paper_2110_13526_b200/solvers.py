@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import csv
 import ctypes
+import functools
 import time
 from dataclasses import dataclass
 
@@ -575,6 +576,22 @@ class CglsRun:
                             self.history, getattr(op, "workers", 1), self.breakdown)
 
 
+def _nvtx(name):
+    """NVTX range around a public solver call (the kernels inside carry the C library's ranges:
+    cbct_project / cbct_backproject / cbct_normal_diagonal)."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapped(*args, **kwargs):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapped
+    return deco
+
+
+@_nvtx("cbct_cgls")
 def cgls(op, b, cfg: SolverConfig) -> SolverReport:
     """CGLS with delayed residual (solvers.py:269-358): K+2 A, K+1 A^T."""
     _check_inputs(op, b, cfg, "cgls")
@@ -770,6 +787,7 @@ class LsqrRun:
             self.breakdown = h[11] == 1.0
 
 
+@_nvtx("cbct_lsqr")
 def lsqr(op, b, cfg: SolverConfig) -> SolverReport:
     """LSQR (solvers.py:361-459): Golub-Kahan bidiagonalisation + Givens.  The fp32 fused chain runs
     device-resident (two fused vector passes per iteration, no host round trip); the fp64 path,
@@ -976,11 +994,13 @@ def _classical(op, b, cfg: SolverConfig, method: str) -> SolverReport:  # solver
     return run.report()
 
 
+@_nvtx("cbct_sirt")
 def sirt(op, b, cfg: SolverConfig) -> SolverReport:
     """SIRT: x += relaxation C^-1 A^T R^-1 (b - A x), optionally clamped (solvers.py:572-578)."""
     return _classical(op, b, cfg, "sirt")
 
 
+@_nvtx("cbct_psirt")
 def psirt(op, b, cfg: SolverConfig) -> SolverReport:
     """PSIRT: scalar step 2*omega/(1.05*rho) (solvers.py:581-587)."""
     return _classical(op, b, cfg, "psirt")
