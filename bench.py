@@ -498,13 +498,10 @@ def run_sharded(args, cfg, rank, world, local_rank):
     if args.p2p:  # fused update + all-gather kernels over NVLink peer memory
         sop.enable_p2p()
     op = sop.op
-    truth = op.phantom_internal(P.shepp_logan_3d())
-    b_full = op.new_projections()
-    op.project_internal(truth, b_full)  # inverse crime b = A phantom; each rank keeps its view block
+    # inverse crime b = A phantom; each rank projects its own view block (rank-local plan)
+    sop._d_full[: op.vol_elems] = op.phantom_internal(P.shepp_logan_3d())
     b_local = torch.zeros(sop.m_loc, device=dev)
-    blk = b_full[sop.v0 * sop.view_elems: sop.v1 * sop.view_elems]
-    b_local[: blk.numel()] = blk
-    del b_full, truth
+    sop.project_local(sop._d_full, b_local)
     vec = CudaVectors(op)
     steps, warmup = args.steps, args.warmup
 

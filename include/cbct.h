@@ -100,6 +100,13 @@ typedef struct cbct_plan_info {
  * Replaces CbctOperator.__init__'s table setup (operator.py:292-301). */
 int cbct_plan_create(cbct_plan** plan, const cbct_geometry* geom, void* stream);
 int cbct_plan_destroy(cbct_plan* plan);
+/* A plan for one rank of the sharded operator: the column table of views
+ * [view0, view1) only (cbct_project_views inside that block) and the cell table of cell rows
+ * [row0, row1) only (cbct_backproject_rows inside that block), so the tables shrink ~1/world.
+ * Within its blocks it computes exactly what the unsharded plan computes (same tables for those
+ * views / rows, same launch shapes).  No fp64 path (cbct_plan_enable_f64 refuses). */
+int cbct_plan_create_shard(cbct_plan** plan, const cbct_geometry* geom, int64_t view0, int64_t view1,
+                           int64_t row0, int64_t row1, void* stream);
 int cbct_plan_get_info(const cbct_plan* plan, cbct_plan_info* info);
 
 /* ---- operators on device buffers (internal layouts) ----------------------- */

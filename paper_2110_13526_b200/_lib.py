@@ -52,6 +52,8 @@ class PlanInfo(ctypes.Structure):
 # name -> (restype, argtypes); every symbol of include/cbct.h
 SIGNATURES = {
     "cbct_plan_create": (c_i32, [ctypes.POINTER(c_p), ctypes.POINTER(Geometry), c_p]),
+    "cbct_plan_create_shard": (c_i32, [ctypes.POINTER(c_p), ctypes.POINTER(Geometry), c_i64, c_i64, c_i64, c_i64,
+                                       c_p]),
     "cbct_plan_destroy": (c_i32, [c_p]),
     "cbct_plan_get_info": (c_i32, [c_p, ctypes.POINTER(PlanInfo)]),
     "cbct_project": (c_i32, [c_p, c_p, c_p, c_p, c_p]),

@@ -635,6 +635,8 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
     if (p && (row0 < 0 || row1 > p->ny || row0 >= row1))
         return cbct_fail(CBCT_E_ARG, "cbct_backproject: bad row range");
     if (!p || !vol || !scratch) return cbct_fail(CBCT_E_ARG, "cbct_backproject: null argument");
+    if (row0 < p->own_r0 || row1 > p->own_r1)
+        return cbct_fail(CBCT_E_ARG, "cbct_backproject: cell rows outside this shard plan's row block");
     if (mode != 1 && mode != 2) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode must be 1 or 2");
     if (mode == 1 && !proj) return cbct_fail(CBCT_E_ARG, "cbct_backproject: mode 1 needs projections");
     cudaStream_t s = (cudaStream_t)stream;

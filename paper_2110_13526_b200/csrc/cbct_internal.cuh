@@ -27,7 +27,7 @@ struct CbctRange {
     CbctRange& operator=(const CbctRange&) = delete;
 };
 
-#define CBCT_CHECK(expr)                                      \
+#define CBCT_CHECK(expr)                                       \
     do {                                                       \
         cudaError_t _e = (expr);                               \
         if (_e != cudaSuccess) return cbct_fail_cuda(_e, #expr); \
@@ -80,6 +80,10 @@ struct cbct_plan {
     int32_t flat_v;     // index of the flat row (|w| < 1e-12 p2) or -1
     // sizes
     int64_t n_cols, n_cells, n_intervals, max_intervals, max_cell_entries;
+    // shard plan (cbct_plan_create_shard): the column table holds views [own_v0, own_v1), the cell
+    // table cell rows [own_r0, own_r1); the unsharded plan owns everything
+    int64_t own_v0 = 0, own_v1 = 0, own_r0 = 0, own_r1 = 0;
+    bool sharded = false;
     int64_t vol_elems, n_rays;
     size_t table_bytes;
     // device tables

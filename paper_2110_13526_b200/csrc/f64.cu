@@ -634,6 +634,7 @@ Grid3 grid3(const cbct_plan* p) {
 // ------------------------------------------------------------------------------ C ABI --
 extern "C" int cbct_plan_enable_f64(cbct_plan* p, void* stream) {
     if (!p) return cbct_fail(CBCT_E_ARG, "cbct_plan_enable_f64: null plan");
+    if (p->sharded) return cbct_fail(CBCT_E_ARG, "cbct_plan_enable_f64: the fp64 path needs an unsharded plan");
     if (p->d_len64) return 0;
     cudaStream_t s = (cudaStream_t)stream;
     const Grid3 g = grid3(p);

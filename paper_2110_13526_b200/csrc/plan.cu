@@ -169,10 +169,73 @@ __global__ void k_column_fill(GeomDev g, const double* srcs, const double* det00
     walk_column(g, sx, sy, rx, ry, h.tmin, h.tmax, [&](double te, int64_t ix, int64_t iy) {
         const int64_t cell = iy * g.nx + ix;
         ent[k] = make_float2((float)(te - tref), __int_as_float((int32_t)(cell * g.zs)));
-        cellkey[k] = (int32_t)cell;
-        colid[k] = (int32_t)c;
+        if (cellkey) {  // full plan: the cell table is sorted out of the column table
+            cellkey[k] = (int32_t)cell;
+            colid[k] = (int32_t)c;
+        }
         ++k;
     });
+}
+
+// Shard plans (cbct_plan_create_shard): the cell table of cell rows [r0, r1) straight from the
+// column walks of ALL columns, without a full column table.  Same fp32 interval ends as
+// k_column_fill + k_cell_entries (tau_a = the previous interval end of the column, or its
+// tau_start), so the shard's cell entries equal the full plan's for those rows bit for bit.
+// FILL = false: count the entries per column and take the straddle statistics of k_max_dtau over
+// every column; FILL = true: write them at off[c] with their cell as the sort key.
+template <bool FILL>
+__global__ void k_cell_walk(GeomDev g, const double* srcs, const double* det00, const double* ustep, int64_t n_cols,
+                            const ColumnHeader* cols, int64_t r0, int64_t r1, int64_t* counts, const int64_t* off,
+                            CellEntry* tmp, int32_t* keys, unsigned int* out_bits, unsigned int* out_tmin) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    const ColumnHeader h = cols[c];
+    int64_t n = 0;
+    if (h.tmax > h.tmin) {  // clip_xy succeeded (k_column_headers)
+        const int64_t view = c / g.nu, u = c - view * g.nu;
+        double sx, sy, rx, ry;
+        column_ray(srcs, det00, ustep, view, u, sx, sy, rx, ry);
+        const double tref = (double)h.t_ref;
+        float prev = h.tau_start, mx = 0.0f;
+        int64_t k = FILL ? off[c] : 0;
+        const int64_t any = walk_column(g, sx, sy, rx, ry, h.tmin, h.tmax, [&](double te, int64_t ix, int64_t iy) {
+            const float x = (float)(te - tref);
+            if (!FILL) mx = fmaxf(mx, x - prev);
+            if (iy >= r0 && iy < r1) {
+                if (FILL) {
+                    CellEntry ce;
+                    ce.vu = (int32_t)c;
+                    ce.tau_a = prev;
+                    ce.tau_b = x;
+                    tmp[k] = ce;
+                    keys[k] = (int32_t)(iy * g.nx + ix);
+                    ++k;
+                } else {
+                    ++n;
+                }
+            }
+            prev = x;
+        });
+        if (!FILL && any) {
+            atomicMax(out_bits, __float_as_uint(mx));
+            atomicMin(out_tmin, __float_as_uint((float)h.tmin));
+        }
+    }
+    if (!FILL) counts[c] = n;
+}
+
+__global__ void k_cell_gather(const int32_t* sorted_idx, int64_t n, const CellEntry* tmp, CellEntry* out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = tmp[(int64_t)(uint32_t)sorted_idx[k]];
+}
+
+// Shard plans keep the column table of views [c0, c1) / nu only; the launch shapes still follow
+// the longest column of the whole geometry (same kernels as the unsharded plan).
+__global__ void k_keep_columns(int64_t* counts, int64_t n_cols, int64_t c0, int64_t c1, unsigned long long* mx) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= n_cols) return;
+    atomicMax(mx, (unsigned long long)counts[c]);
+    if (c < c0 || c >= c1) counts[c] = 0;
 }
 
 __global__ void k_cell_entries(const int32_t* sorted_idx, int64_t n, const float2* ent, const int32_t* colid,
@@ -288,13 +351,18 @@ extern "C" int cbct_plan_destroy(cbct_plan* p) {
     return 0;
 }
 
-extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* stream_) {
-    CbctRange range("cbct_plan_create");
+// v0..v1: views whose column table (A) the plan keeps; r0..r1: cell rows whose cell table (A^T)
+// it keeps.  The unsharded plan keeps all of both.
+static int plan_create(cbct_plan** out, const cbct_geometry* g, int64_t v0, int64_t v1, int64_t r0, int64_t r1,
+                       void* stream_) {
     if (!out || !g || !g->srcs || !g->det00 || !g->ustep || !g->vstep)
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: null argument");
     *out = nullptr;
     if (g->nx < 1 || g->ny < 1 || g->nz < 1 || g->nu < 1 || g->nv < 1 || g->n_views < 1)
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: counts must be >= 1");
+    if (v0 < 0 || v1 > g->n_views || v0 >= v1 || r0 < 0 || r1 > g->ny || r0 >= r1)
+        return cbct_fail(CBCT_E_ARG, "cbct_plan_create_shard: empty or out-of-range view / row block");
+    const bool shard = v0 > 0 || v1 < g->n_views || r0 > 0 || r1 < g->ny;
     if (!(g->pitch[0] > 0 && g->pitch[1] > 0 && g->pitch[2] > 0))
         return cbct_fail(CBCT_E_ARG, "cbct_plan_create: voxel pitch must be > 0");
     const int64_t zs = (g->nz + 2 * CBCT_ZPAD + 3) / 4 * 4;  // 16-B aligned cell columns (TMA)
@@ -338,6 +406,8 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     }
     p->n_cols = V * g->nu;
     p->n_cells = g->nx * g->ny;
+    p->own_v0 = v0; p->own_v1 = v1; p->own_r0 = r0; p->own_r1 = r1;
+    p->sharded = shard;
     p->vol_elems = p->n_cells * zs;
     p->n_rays = p->n_cols * g->nv;
     size_t total = 0;
@@ -349,6 +419,9 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
             *d_idx_sorted = nullptr;
     void* d_tmp = nullptr;
     unsigned long long* d_max = nullptr;
+    unsigned int* d_bits = nullptr;
+    int64_t *d_ccount = nullptr, *d_coff = nullptr;
+    CellEntry* d_ctmp = nullptr;
 
 #define TRY(x) do { rc = (x); if (rc) goto fail; } while (0)
 #define TRYC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { rc = cbct_fail_cuda(_e, #x); goto fail; } } while (0)
@@ -377,6 +450,21 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
                                                                          flat_w, p->flat_v, g->lo[2], g->pitch[2],
                                                                          g->nz, p->d_cols, d_counts);
         TRYC(cudaGetLastError());
+        // d_max: longest column list, longest cell list, (shard) longest column list of all views;
+        // d_bits: straddle statistics (max interval, min t) over every column
+        TRY(dev_alloc(&d_max, 3, nullptr));
+        TRYC(cudaMemsetAsync(d_max, 0, 3 * sizeof(unsigned long long), stream));
+        TRY(dev_alloc(&d_bits, 2, nullptr));
+        {
+            const unsigned int init[2] = {0u, 0x7f7fffffu};
+            TRYC(cudaMemcpyAsync(d_bits, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+            TRYC(cudaStreamSynchronize(stream));
+        }
+        if (shard) {
+            k_keep_columns<<<blocks_for(p->n_cols, 256), 256, 0, stream>>>(d_counts, p->n_cols, v0 * g->nu,
+                                                                           v1 * g->nu, d_max + 2);
+            TRYC(cudaGetLastError());
+        }
         size_t tmp_bytes = 0;
         TRYC(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_counts, p->d_col_off, p->n_cols + 1, stream));
         TRYC(cudaMalloc(&d_tmp, tmp_bytes));
@@ -389,37 +477,90 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         if (n >= (int64_t)UINT32_MAX) { rc = cbct_fail(CBCT_E_GEOMETRY, "too many fan-beam intervals"); goto fail; }
 
         TRY(dev_alloc(&p->d_col_ent, n, &total));
-        TRY(dev_alloc(&d_cellkey, n, nullptr));
-        TRY(dev_alloc(&d_colid, n, nullptr));
-        k_column_fill<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(gd, d_srcs, d_det00, d_ustep, p->n_cols,
-                                                                      p->d_cols, p->d_col_off, p->d_col_ent,
-                                                                      d_cellkey, d_colid);
-        TRYC(cudaGetLastError());
-
-        // cell-major order: stable radix sort of entry indices by cell (keeps column order per cell)
-        TRY(dev_alloc(&d_idx, n, nullptr));
-        TRY(dev_alloc(&d_idx_sorted, n, nullptr));
-        TRY(dev_alloc(&d_keys_sorted, n, nullptr));
-        k_iota<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx, n);
-        TRYC(cudaGetLastError());
         int end_bit = 1;
         while ((int64_t(1) << end_bit) <= p->n_cells) ++end_bit;
-        tmp_bytes = 0;
-        TRYC(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
-                                             (int64_t)n, 0, end_bit, stream));
-        TRYC(cudaMalloc(&d_tmp, tmp_bytes));
-        TRYC(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
-                                             (int64_t)n, 0, end_bit, stream));
-        cudaFree(d_tmp); d_tmp = nullptr;
+        if (!shard) {
+            TRY(dev_alloc(&d_cellkey, n, nullptr));
+            TRY(dev_alloc(&d_colid, n, nullptr));
+            k_column_fill<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(gd, d_srcs, d_det00, d_ustep, p->n_cols,
+                                                                          p->d_cols, p->d_col_off, p->d_col_ent,
+                                                                          d_cellkey, d_colid);
+            TRYC(cudaGetLastError());
 
-        TRY(dev_alloc(&p->d_cell_ent, n, &total));
-        TRY(dev_alloc(&p->d_cell_off, p->n_cells + 1, &total));
-        k_cell_entries<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx_sorted, n, p->d_col_ent, d_colid,
-                                                               p->d_col_off, p->d_cols, p->d_cell_ent);
-        TRYC(cudaGetLastError());
-        k_cell_offsets<<<blocks_for(p->n_cells + 1, 256), 256, 0, stream>>>(d_keys_sorted, n, p->n_cells,
-                                                                            p->d_cell_off);
-        TRYC(cudaGetLastError());
+            // cell-major order: stable radix sort of entry indices by cell (keeps column order per cell)
+            TRY(dev_alloc(&d_idx, n, nullptr));
+            TRY(dev_alloc(&d_idx_sorted, n, nullptr));
+            TRY(dev_alloc(&d_keys_sorted, n, nullptr));
+            k_iota<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx, n);
+            TRYC(cudaGetLastError());
+            tmp_bytes = 0;
+            TRYC(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                                 (int64_t)n, 0, end_bit, stream));
+            TRYC(cudaMalloc(&d_tmp, tmp_bytes));
+            TRYC(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                                 (int64_t)n, 0, end_bit, stream));
+            cudaFree(d_tmp); d_tmp = nullptr;
+
+            TRY(dev_alloc(&p->d_cell_ent, n, &total));
+            TRY(dev_alloc(&p->d_cell_off, p->n_cells + 1, &total));
+            k_cell_entries<<<blocks_for(n, 256), 256, 0, stream>>>(d_idx_sorted, n, p->d_col_ent, d_colid,
+                                                                   p->d_col_off, p->d_cols, p->d_cell_ent);
+            TRYC(cudaGetLastError());
+            k_cell_offsets<<<blocks_for(p->n_cells + 1, 256), 256, 0, stream>>>(d_keys_sorted, n, p->n_cells,
+                                                                                p->d_cell_off);
+            TRYC(cudaGetLastError());
+            k_max_dtau<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(p->d_col_ent, p->d_col_off, p->d_cols,
+                                                                       p->n_cols, d_bits, d_bits + 1);
+            TRYC(cudaGetLastError());
+        } else {
+            k_column_fill<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(gd, d_srcs, d_det00, d_ustep, p->n_cols,
+                                                                          p->d_cols, p->d_col_off, p->d_col_ent,
+                                                                          nullptr, nullptr);
+            TRYC(cudaGetLastError());
+            // cell rows [r0, r1): count per column (and the straddle statistics of all columns),
+            // scan, fill in column order, stable sort by cell -- the full plan's cell order
+            TRY(dev_alloc(&d_ccount, p->n_cols + 1, nullptr));
+            TRY(dev_alloc(&d_coff, p->n_cols + 1, nullptr));
+            TRYC(cudaMemsetAsync(d_ccount, 0, (p->n_cols + 1) * sizeof(int64_t), stream));
+            k_cell_walk<false><<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(
+                gd, d_srcs, d_det00, d_ustep, p->n_cols, p->d_cols, r0, r1, d_ccount, nullptr, nullptr, nullptr, d_bits,
+                d_bits + 1);
+            TRYC(cudaGetLastError());
+            tmp_bytes = 0;
+            TRYC(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_ccount, d_coff, p->n_cols + 1, stream));
+            TRYC(cudaMalloc(&d_tmp, tmp_bytes));
+            TRYC(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_ccount, d_coff, p->n_cols + 1, stream));
+            cudaFree(d_tmp); d_tmp = nullptr;
+            int64_t nr = 0;
+            TRYC(cudaMemcpyAsync(&nr, d_coff + p->n_cols, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+            TRYC(cudaStreamSynchronize(stream));
+            if (nr >= (int64_t)UINT32_MAX) { rc = cbct_fail(CBCT_E_GEOMETRY, "too many fan-beam intervals"); goto fail; }
+            TRY(dev_alloc(&d_ctmp, nr, nullptr));
+            TRY(dev_alloc(&d_cellkey, nr, nullptr));
+            k_cell_walk<true><<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(
+                gd, d_srcs, d_det00, d_ustep, p->n_cols, p->d_cols, r0, r1, nullptr, d_coff, d_ctmp, d_cellkey, nullptr,
+                nullptr);
+            TRYC(cudaGetLastError());
+            TRY(dev_alloc(&d_idx, nr, nullptr));
+            TRY(dev_alloc(&d_idx_sorted, nr, nullptr));
+            TRY(dev_alloc(&d_keys_sorted, nr, nullptr));
+            k_iota<<<blocks_for(nr, 256), 256, 0, stream>>>(d_idx, nr);
+            TRYC(cudaGetLastError());
+            tmp_bytes = 0;
+            TRYC(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                                 nr, 0, end_bit, stream));
+            TRYC(cudaMalloc(&d_tmp, tmp_bytes));
+            TRYC(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_cellkey, d_keys_sorted, d_idx, d_idx_sorted,
+                                                 nr, 0, end_bit, stream));
+            cudaFree(d_tmp); d_tmp = nullptr;
+            TRY(dev_alloc(&p->d_cell_ent, nr, &total));
+            TRY(dev_alloc(&p->d_cell_off, p->n_cells + 1, &total));
+            k_cell_gather<<<blocks_for(nr, 256), 256, 0, stream>>>(d_idx_sorted, nr, d_ctmp, p->d_cell_ent);
+            TRYC(cudaGetLastError());
+            k_cell_offsets<<<blocks_for(p->n_cells + 1, 256), 256, 0, stream>>>(d_keys_sorted, nr, p->n_cells,
+                                                                                p->d_cell_off);
+            TRYC(cudaGetLastError());
+        }
         // A^T in view batches once the ray-prefix table outgrows half of L2: 2 up to 4 GiB, then one
         // per 2 GiB up to 4 (measured: config 2 14.75 -> 14.46 ms with 2, 3-8 batches slower; config
         // 3 131.9 -> 127.6 ms with 2, 128.9 with 4; config 5 (9 GB) G=6 1965 ms -> 1679 with 4-6, 1684
@@ -438,25 +579,16 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
             TRYC(cudaGetLastError());
         }
 
-        TRY(dev_alloc(&d_max, 2, nullptr));
-        TRYC(cudaMemsetAsync(d_max, 0, 2 * sizeof(unsigned long long), stream));
         k_max_span<<<blocks_for(p->n_cols, 256), 256, 0, stream>>>(p->d_col_off, p->n_cols, d_max);
         k_max_span<<<blocks_for(p->n_cells, 256), 256, 0, stream>>>(p->d_cell_off, p->n_cells, d_max + 1);
-        unsigned long long mx[2];
+        unsigned long long mx[3];
         TRYC(cudaMemcpyAsync(mx, d_max, sizeof(mx), cudaMemcpyDeviceToHost, stream));
 
         {
             // straddle bound for the boundary-form backprojector (backproject.cu)
-            unsigned int* d_bits = nullptr;
-            TRYC(cudaMalloc(&d_bits, 2 * sizeof(unsigned int)));
-            unsigned int init[2] = {0u, 0x7f7fffffu};
-            TRYC(cudaMemcpyAsync(d_bits, init, sizeof(init), cudaMemcpyHostToDevice, stream));
-            k_max_dtau<<<blocks_for(p->n_cols, 128), 128, 0, stream>>>(p->d_col_ent, p->d_col_off, p->d_cols,
-                                                                       p->n_cols, d_bits, d_bits + 1);
             unsigned int hb[2];
             TRYC(cudaMemcpyAsync(hb, d_bits, sizeof(hb), cudaMemcpyDeviceToHost, stream));
             TRYC(cudaStreamSynchronize(stream));
-            cudaFree(d_bits);
             float mx, tmin_f;
             memcpy(&mx, &hb[0], 4);
             memcpy(&tmin_f, &hb[1], 4);
@@ -484,7 +616,9 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
         k_row_tables<<<blocks_for(g->nv, 128), 128, 0, stream>>>(g->nv, det00z, pv, g->pitch[2], p->d_w, p->d_invw);
         TRYC(cudaGetLastError());
         TRYC(cudaStreamSynchronize(stream));
-        p->max_intervals = (int64_t)mx[0];
+        // a shard plan sizes the projector for the longest column of ALL views (the same launch
+        // shapes, hence the same results, as the unsharded plan)
+        p->max_intervals = (int64_t)(shard ? mx[2] : mx[0]);
         p->max_cell_entries = (int64_t)mx[1];
     }
     cbct_count_launch(9);
@@ -591,16 +725,31 @@ extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* s
     p->table_bytes = total;
     cudaFree(d_counts); cudaFree(d_cellkey);  // d_srcs/d_det00/d_ustep belong to the plan
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
+    cudaFree(d_bits); cudaFree(d_ccount); cudaFree(d_coff); cudaFree(d_ctmp);
     *out = p;
     return 0;
 fail:
     cudaFree(d_counts); cudaFree(d_cellkey);  // d_srcs/d_det00/d_ustep belong to the plan
     cudaFree(d_colid); cudaFree(d_keys_sorted); cudaFree(d_idx); cudaFree(d_idx_sorted); cudaFree(d_max);
+    cudaFree(d_bits); cudaFree(d_ccount); cudaFree(d_coff); cudaFree(d_ctmp);
     cudaFree(d_tmp);
     cbct_plan_destroy(p);
     return rc;
 #undef TRY
 #undef TRYC
+}
+
+extern "C" int cbct_plan_create(cbct_plan** out, const cbct_geometry* g, void* stream) {
+    CbctRange range("cbct_plan_create");
+    if (!g) return cbct_fail(CBCT_E_ARG, "cbct_plan_create: null argument");
+    return plan_create(out, g, 0, g->n_views, 0, g->ny, stream);
+}
+
+extern "C" int cbct_plan_create_shard(cbct_plan** out, const cbct_geometry* g, int64_t view0, int64_t view1,
+                                      int64_t row0, int64_t row1, void* stream) {
+    CbctRange range("cbct_plan_create_shard");
+    if (!g) return cbct_fail(CBCT_E_ARG, "cbct_plan_create_shard: null argument");
+    return plan_create(out, g, view0, view1, row0, row1, stream);
 }
 
 extern "C" int cbct_plan_get_info(const cbct_plan* p, cbct_plan_info* info) {

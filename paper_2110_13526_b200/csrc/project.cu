@@ -522,6 +522,8 @@ extern "C" int cbct_project_views(const cbct_plan* p, const float* vol, float* p
     CbctRange range("cbct_project");
     if (!p || !vol || !proj) return cbct_fail(CBCT_E_ARG, "cbct_project: null argument");
     if (view0 < 0 || view1 > p->V || view0 >= view1) return cbct_fail(CBCT_E_ARG, "cbct_project: bad view range");
+    if (view0 < p->own_v0 || view1 > p->own_v1)
+        return cbct_fail(CBCT_E_ARG, "cbct_project: views outside this shard plan's view block");
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t c0 = view0 * p->nu;
     const dim3 grid((unsigned)((view1 - view0) * p->nu));

@@ -155,10 +155,18 @@ class ShardedOperator:
 
         self.comm = comm
         self.world, self.rank = comm.world, comm.rank
-        self.op = CbctOperator(vol_geom, trajectory, device=device)
+        self.layout = L = ShardLayout(vol_geom, trajectory, self.world, self.rank)
+        # rank-local plan: the column table of this rank's views and the cell table of its cell
+        # rows only (~1/world of the tables, cbct_plan_create_shard).  An empty block (more ranks
+        # than views or rows) keeps one item, which is never launched.
+        V, ny = trajectory.n_views, vol_geom.ny
+        sv0 = min(L.v0, V - 1)
+        sy0 = min(L.y0, ny - 1)
+        shard = (sv0, max(L.v1, sv0 + 1), sy0, max(L.y1, sy0 + 1))
+        full = shard == (0, V, 0, ny)
+        self.op = CbctOperator(vol_geom, trajectory, device=device, _shard=None if full else shard)
         self.device = self.op.device
         det = trajectory.detector
-        self.layout = L = ShardLayout(vol_geom, trajectory, self.world, self.rank)
         assert L.zs == self.op.zstride
         self.v0, self.v1, vper = L.v0, L.v1, L.vper
         self.y0, self.y1, yper = L.y0, L.y1, L.yper

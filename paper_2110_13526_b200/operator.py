@@ -99,7 +99,7 @@ class CbctOperator:
     deterministic gather, so results are bitwise reproducible for any value.
     """
 
-    def __init__(self, vol_geom, trajectory, workers: int = 8, device=None, precision: str = "f32"):
+    def __init__(self, vol_geom, trajectory, workers: int = 8, device=None, precision: str = "f32", _shard=None):
         if workers < 1:
             raise ValueError("workers must be >= 1")
         if precision not in PRECISIONS:
@@ -129,8 +129,17 @@ class CbctOperator:
         g.nu, g.nv, g.n_views = det.nu, det.nv, trajectory.n_views
         g.srcs, g.det00, g.ustep, g.vstep = (a.ctypes.data for a in self._tables)
         plan = ctypes.c_void_p()
+        # _shard = (view0, view1, row0, row1): a rank-local plan of the sharded operator
+        # (distributed.ShardedOperator), which only supports A on those views and A^T on those
+        # cell rows (cbct_plan_create_shard)
+        self.shard = None if _shard is None else tuple(int(v) for v in _shard)
+        if self.shard is not None and precision != "f32":
+            raise ValueError("a shard plan has no fp64 path")
         with torch.cuda.device(self.device):
-            call("cbct_plan_create", ctypes.byref(plan), ctypes.byref(g), self._stream())
+            if self.shard is None:
+                call("cbct_plan_create", ctypes.byref(plan), ctypes.byref(g), self._stream())
+            else:
+                call("cbct_plan_create_shard", ctypes.byref(plan), ctypes.byref(g), *self.shard, self._stream())
         self._plan = plan
         if self.f64:
             with torch.cuda.device(self.device):

@@ -56,6 +56,73 @@ def test_sharded_kernels_assemble_to_full(world):
     assert torch.equal(r_cat, r_full)
 
 
+@pytest.mark.parametrize("world", [3, 8])
+def test_shard_plans_at_config3_geometry(world):
+    """Rank-local plans (cbct_plan_create_shard) at BASELINE config-3 cell and detector sizes on a
+    view subset and a z slab, where A^T runs the sided kernel: every rank's A on its views and
+    A^T / diag(A^T A) on its cell rows reassemble bit-for-bit to the unsharded plan, and each
+    rank's tables are ~1/world of the unsharded plan's (column table of its views, cell table of
+    its rows)."""
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200.distributed import ShardedOperator
+
+    vg, tr = baseline_geometry(512, 720, 616, 480, views=(100, 24), zslab=(224, 64))
+    full = P.CbctOperator(vg, tr)
+    assert full.info.bp_sided_gs > 0
+    x = full.volume_to_internal(P.generate_phantom(P.shepp_logan_3d(), vg).data)
+    y = torch.randn(full.m, device="cuda")
+    p_full, r_full, d_full = full.new_projections(), full.new_volume(), full.new_volume()
+    full.project_internal(x, p_full)
+    full.backproject_internal(y, r_full)
+    full.backproject_internal(None, d_full, mode=2)
+    parts = {"p": [], "r": [], "d": []}
+    for rank in range(world):
+        sop = ShardedOperator(vg, tr, _VirtualComm(world, rank))
+        assert sop.op.shard is not None
+        info = sop.op.info
+        assert (info.proj_chunk, info.bp_groups, info.bp_view_batches, info.bp_sided_gs) == (
+            full.info.proj_chunk, full.info.bp_groups, full.info.bp_view_batches, full.info.bp_sided_gs)
+        # the column + cell tables scale with the shard; per-column headers and offsets do not
+        assert info.table_bytes <= full.info.table_bytes * (1.0 / world + 0.12), (rank, info.table_bytes)
+        dd = torch.zeros(sop.n_full, device="cuda")
+        dd[: full.vol_elems] = x
+        ee = torch.zeros(sop.m_full, device="cuda")
+        ee[: full.m] = y
+        p_loc = torch.zeros(sop.m_loc, device="cuda")
+        r_loc, d_loc = torch.zeros(sop.n_loc, device="cuda"), torch.zeros(sop.n_loc, device="cuda")
+        sop.project_local(dd, p_loc)
+        sop.backproject_local(ee, r_loc)
+        sop.backproject_local(None, d_loc, mode=2)
+        parts["p"].append(p_loc)
+        parts["r"].append(r_loc)
+        parts["d"].append(d_loc)
+    assert torch.equal(torch.cat(parts["p"])[: full.m], p_full)
+    assert torch.equal(torch.cat(parts["r"])[: full.vol_elems], r_full)
+    assert torch.equal(torch.cat(parts["d"])[: full.vol_elems], d_full)
+
+
+def test_shard_plan_refuses_outside_its_blocks():
+    import ctypes
+
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200._lib import CbctError, call
+
+    vg, tr = baseline_geometry(64, 90, 128, 96)
+    op = P.CbctOperator(vg, tr, _shard=(30, 60, 16, 40))
+    vol, proj = op.new_volume(), op.new_projections()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    with pytest.raises(CbctError, match="view block"):
+        call("cbct_project_views", op._plan, ctypes.c_void_p(vol.data_ptr()), ctypes.c_void_p(proj.data_ptr()),
+             0, 60, None, s)
+    with pytest.raises(CbctError, match="row block"):
+        call("cbct_backproject_rows", op._plan, ctypes.c_void_p(proj.data_ptr()), ctypes.c_void_p(vol.data_ptr()),
+             10, 40, 1, ctypes.c_void_p(op.new_bp_scratch().data_ptr()), None, None, s)
+    with pytest.raises(CbctError, match="view block"):
+        op.project_internal(vol, proj)  # the whole-operator entry point needs every view
+    with pytest.raises(ValueError, match="fp64"):
+        P.CbctOperator(vg, tr, precision="f64", _shard=(0, 45, 0, 64))
+
+
 def test_nccl_world1_driver_matches_cgls():
     import torch.distributed as dist
 
