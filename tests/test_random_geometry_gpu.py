@@ -87,3 +87,23 @@ def test_random_geometry_against_oracle(seed, monkeypatch):
     assert rel_l2(got, want) <= 2e-5, (plan, "A^T rel-L2", rel_l2(got, want))
     got, want = op.normal_diagonal().data, ref.normal_diagonal()
     assert max_rel(got, want) <= TOL, (plan, "normal_diagonal", max_rel(got, want))
+
+
+@pytest.mark.parametrize("seed", range(0, 24, 3))
+def test_random_geometry_f64_path(seed):
+    """The reference-precision path (csrc/f64.cu) on the same geometries: A bit for bit the
+    oracle's (the reference's fp64 Siddon sum, operator.py:190-206), A^T and diag(A^T A) to
+    fp64 summation-order rounding."""
+    from paper_2110_13526_b200.operator import CbctOperator, ProjectionStack
+    from paper_2110_13526_b200.phantom import Volume
+
+    vg, tr = _geometry(seed)
+    op, ref = CbctOperator(vg, tr, precision="f64"), O.OracleOperator(vg, tr)
+    x = np.random.default_rng(seed).random(op.n)
+    y = np.random.default_rng(seed + 1).standard_normal(op.m)
+    got, want = op.project(Volume(vg, x)).data, ref.project(x)
+    assert np.array_equal(got, want), (seed, max_rel(got, want))
+    got, want = op.backproject(ProjectionStack(tr, y)).data, ref.backproject(y)
+    assert max_rel(got, want) <= 1e-13, (seed, max_rel(got, want))
+    got, want = op.normal_diagonal().data, ref.normal_diagonal()
+    assert max_rel(got, want) <= 1e-13, (seed, max_rel(got, want))
