@@ -188,12 +188,15 @@ __global__ void __launch_bounds__(512) k_bp_direct(const int64_t* __restrict__ c
 // halves the bytes per boundary lookup.  The flat row (if any) is kept out of P
 // and stored in flatw[c].
 // squared (mode 2): yw = |r|^2 (y ignored), the weights of diag(A^T A)'s boundary form (k_bp_sided).
+// colidx (shard plans): only the listed columns, the ones crossing the plan's cell rows.
 __global__ void k_prefix_rays(const ColumnHeader* __restrict__ cols, const double* __restrict__ wtab,
                               const float* __restrict__ y, float* __restrict__ pref, float* __restrict__ flatw,
-                              int64_t n_cols, int nv, int flat_v, int pad_lo, int pad_hi, int squared = 0) {
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                              int64_t n_cols, int nv, int flat_v, int pad_lo, int pad_hi, int squared = 0,
+                              const int32_t* __restrict__ colidx = nullptr) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (c >= n_cols) return;
+    if (i >= n_cols) return;
+    const int64_t c = colidx ? (int64_t)colidx[i] : i;
     const float rxy2 = (float)cols[c].rxy2;
     const float* yc = y + c * nv;
     const int nvq = nv + 2 + pad_lo + pad_hi;
@@ -655,10 +658,15 @@ extern "C" int cbct_backproject_rows(const cbct_plan* p, const float* proj, floa
         float* pyb = scratch;
         const int nvq = (int)p->nv + 2 + p->bp_pad_lo + p->bp_pad_hi;
         float* flatw = scratch + p->n_cols * nvq * kPrefWords;
-        const int64_t nthreads = p->n_cols * 32;
-        k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p->d_cols, p->d_w, proj, pyb, flatw,
-                                                                           p->n_cols, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi,
-                                                                           mode == 2 ? 1 : 0);
+        // shard plans: the prefix of the columns crossing the plan's rows only (the others are never read)
+        static const bool pref_all = getenv("CBCT_BP_PREF_ALL") != nullptr;
+        const bool listed = p->d_pref_cols && !pref_all;
+        const int64_t ncp = listed ? p->n_pref_cols : p->n_cols;
+        const int64_t nthreads = ncp * 32;
+        if (ncp > 0)
+            k_prefix_rays<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(
+                p->d_cols, p->d_w, proj, pyb, flatw, ncp, (int)p->nv, p->flat_v, p->bp_pad_lo, p->bp_pad_hi,
+                mode == 2 ? 1 : 0, listed ? p->d_pref_cols : nullptr);
         CBCT_CHECK(cudaGetLastError());
         // closed-form straddle fraction unless the cells are long relative to the source distance
         static const bool force_table = getenv("CBCT_BP_TABLE") != nullptr;

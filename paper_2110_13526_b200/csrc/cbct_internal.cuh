@@ -84,6 +84,8 @@ struct cbct_plan {
     // table cell rows [own_r0, own_r1); the unsharded plan owns everything
     int64_t own_v0 = 0, own_v1 = 0, own_r0 = 0, own_r1 = 0;
     bool sharded = false;
+    int32_t* d_pref_cols = nullptr;  // shard plan: columns with entries in the plan's cell rows (A^T prefix)
+    int64_t n_pref_cols = 0;
     int64_t vol_elems, n_rays;
     size_t table_bytes;
     // device tables

@@ -224,6 +224,11 @@ __global__ void k_cell_walk(GeomDev g, const double* srcs, const double* det00, 
     if (!FILL) counts[c] = n;
 }
 
+__global__ void k_flag_positive(const int64_t* counts, int64_t n, char* flags) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) flags[k] = counts[k] > 0;
+}
+
 __global__ void k_cell_gather(const int32_t* sorted_idx, int64_t n, const CellEntry* tmp, CellEntry* out) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k < n) out[k] = tmp[(int64_t)(uint32_t)sorted_idx[k]];
@@ -337,6 +342,7 @@ extern "C" int cbct_plan_destroy(cbct_plan* p) {
     cudaFree(p->d_cell_off);
     cudaFree(p->d_cell_boff);
     cudaFree(p->d_cell_ent);
+    cudaFree(p->d_pref_cols);
     cudaFree(p->d_w);
     cudaFree(p->d_invw);
     cudaFree(p->d_srcs);
@@ -531,6 +537,30 @@ static int plan_create(cbct_plan** out, const cbct_geometry* g, int64_t v0, int6
             TRYC(cudaMalloc(&d_tmp, tmp_bytes));
             TRYC(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_ccount, d_coff, p->n_cols + 1, stream));
             cudaFree(d_tmp); d_tmp = nullptr;
+            {
+                // the columns with entries in rows [r0, r1): the only prefix rows this plan's A^T reads
+                TRY(dev_alloc(&p->d_pref_cols, p->n_cols, &total));
+                char* d_flags = nullptr;
+                int64_t* d_nsel = nullptr;
+                TRYC(cudaMalloc(&d_flags, p->n_cols));
+                TRYC(cudaMalloc(&d_nsel, sizeof(int64_t)));
+                k_flag_positive<<<blocks_for(p->n_cols, 256), 256, 0, stream>>>(d_ccount, p->n_cols, d_flags);
+                cub::CountingInputIterator<int32_t> ids(0);
+                tmp_bytes = 0;
+                cudaError_t e1 = cub::DeviceSelect::Flagged(nullptr, tmp_bytes, ids, d_flags, p->d_pref_cols, d_nsel,
+                                                            p->n_cols, stream);
+                if (e1 == cudaSuccess) e1 = cudaMalloc(&d_tmp, tmp_bytes);
+                if (e1 == cudaSuccess)
+                    e1 = cub::DeviceSelect::Flagged(d_tmp, tmp_bytes, ids, d_flags, p->d_pref_cols, d_nsel, p->n_cols,
+                                                    stream);
+                if (e1 == cudaSuccess)
+                    e1 = cudaMemcpyAsync(&p->n_pref_cols, d_nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
+                if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(stream);
+                cudaFree(d_flags);
+                cudaFree(d_nsel);
+                cudaFree(d_tmp); d_tmp = nullptr;
+                if (e1 != cudaSuccess) { rc = cbct_fail_cuda(e1, "shard plan column list"); goto fail; }
+            }
             int64_t nr = 0;
             TRYC(cudaMemcpyAsync(&nr, d_coff + p->n_cols, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
             TRYC(cudaStreamSynchronize(stream));
