@@ -101,6 +101,37 @@ def test_shard_plans_at_config3_geometry(world):
     assert torch.equal(torch.cat(parts["d"])[: full.vol_elems], d_full)
 
 
+def test_shard_plans_with_empty_blocks():
+    """More ranks than views and than cell rows: the empty ranks still build a (one-item) plan and
+    contribute nothing; the others reassemble the unsharded A, A^T bit for bit."""
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200.distributed import ShardedOperator
+
+    vg = P.VolumeGeometry(12, 3, 10, (2.0, 2.0, 2.0))
+    tr = P.make_circular_trajectory(300.0, 500.0, 3, 0.1, 2.0, P.DetectorGeometry(20, 15, (3.0, 3.0)))
+    full = P.CbctOperator(vg, tr)
+    x = full.volume_to_internal(np.random.default_rng(0).random(full.n))
+    y = torch.randn(full.m, device="cuda")
+    p_full, r_full = full.new_projections(), full.new_volume()
+    full.project_internal(x, p_full)
+    full.backproject_internal(y, r_full)
+    world = 4
+    p_parts, r_parts = [], []
+    for rank in range(world):
+        sop = ShardedOperator(vg, tr, _VirtualComm(world, rank))
+        dd = torch.zeros(sop.n_full, device="cuda")
+        dd[: full.vol_elems] = x
+        ee = torch.zeros(sop.m_full, device="cuda")
+        ee[: full.m] = y
+        p_loc, r_loc = torch.zeros(sop.m_loc, device="cuda"), torch.zeros(sop.n_loc, device="cuda")
+        sop.project_local(dd, p_loc)
+        sop.backproject_local(ee, r_loc)
+        p_parts.append(p_loc)
+        r_parts.append(r_loc)
+    assert torch.equal(torch.cat(p_parts)[: full.m], p_full)
+    assert torch.equal(torch.cat(r_parts)[: full.vol_elems], r_full)
+
+
 def test_shard_plan_refuses_outside_its_blocks():
     import ctypes
 
