@@ -190,12 +190,13 @@ class CbctOperator:
 
     def __deepcopy__(self, memo):
         # sklearn.clone deep-copies estimators (test_estimators.py:35-43): rebuild the plan.
-        return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device, self.precision)
+        return CbctOperator(self.vol_geom, self.trajectory, self.workers, self.device, self.precision, self.shard)
 
     def __reduce__(self):
         # pickling (joblib workers of sklearn model selection) carries the geometry; the device
         # plan is rebuilt on load
-        return (CbctOperator, (self.vol_geom, self.trajectory, self.workers, str(self.device), self.precision))
+        return (CbctOperator, (self.vol_geom, self.trajectory, self.workers, str(self.device), self.precision,
+                               self.shard))
 
     @property
     def f64(self) -> bool:
