@@ -29,7 +29,7 @@ import torch
 
 from . import hostcopy
 from ._lib import call
-from .solvers import ConvergenceRecord, SolverReport, SolverConfig
+from .solvers import ConvergenceRecord, SolverReport, SolverConfig, _nvtx
 
 __all__ = ["block", "ShardLayout", "ShardedOperator", "CudaVectors", "TorchComm", "DistCglsRun", "dist_cgls",
            "DistLsqrRun", "dist_lsqr", "DistClassicalRun", "dist_psirt", "dist_sirt", "gathered_report"]
@@ -309,6 +309,7 @@ class DistCglsRun:
         return not self.done and self.rel(self.nb) > self.cfg.rel_discrepancy_tol and \
             self.i < self.cfg.max_iterations
 
+    @_nvtx("cbct_dist_cgls_iteration")
     def step(self) -> bool:
         sop, vec = self.sop, self.vec
         nr2 = self.allsum(sop.backproject_local(sop.gather_proj(self.e), self.r, norm2=True))
@@ -330,6 +331,7 @@ class DistCglsRun:
         return True
 
     # ------------------------------------------------- device-resident iterations --
+    @_nvtx("cbct_dist_cgls_device_iterations")
     def run_device(self, k: int) -> None:
         """Up to k iterations with every scalar on the device (NCCL + libcbct only): the local norm
         partials are reduced into device scalars, all-gathered (8 bytes per rank) and summed in rank
@@ -493,6 +495,7 @@ class DistLsqrRun:
     def should_continue(self):
         return not self.done and self.updates < self.cfg.max_iterations + 1
 
+    @_nvtx("cbct_dist_lsqr_iteration")
     def step(self) -> None:
         vec, u, v = self.vec, self.u, self.v
         alpha = self.alpha
@@ -627,6 +630,7 @@ class DistClassicalRun:
         err = self.cfg.rel_discrepancy_tol
         return (err == 0.0 or self.e > err) and self.i < self.cfg.max_iterations
 
+    @_nvtx("cbct_dist_classical_iteration")
     def step(self) -> None:
         sop, vec = self.sop, self.vec
         vec.mul(self.resid, self.inv_row, self.weighted)

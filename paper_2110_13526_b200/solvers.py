@@ -404,6 +404,21 @@ def _want_true(cfg, iteration):
     return k > 0 and iteration % k == 0
 
 
+def _nvtx(name):
+    """NVTX range around a public solver call (the kernels inside carry the C library's ranges:
+    cbct_project / cbct_backproject / cbct_normal_diagonal)."""
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapped(*args, **kwargs):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapped
+    return deco
+
+
 class CglsRun:
     """Device-resident CGLS state (solvers.py:269-358), split into the pre-loop
     (``__init__``: 2 A + 1 A^T, first update folded in) and one loop iteration
@@ -474,6 +489,7 @@ class CglsRun:
         return (not self.done) and self.rel(self.nb_full) > self.cfg.rel_discrepancy_tol and \
             self.i < self.cfg.max_iterations
 
+    @_nvtx("cbct_cgls_iteration")
     def step(self, record: bool = True) -> bool:
         """One loop iteration; returns False on breakdown (state left as the reference leaves it)."""
         dev, chain = self.dev, self.chain
@@ -524,6 +540,7 @@ class CglsRun:
         op.reduce_to(dev.nblocks(self.e.numel()), S[5:6])
         call("cbct_cgls_scalars", _p(S), 3, st())                                   # history, tolerance
 
+    @_nvtx("cbct_cgls_device_iterations")
     def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
         """Up to k loop iterations with alpha, beta, the norms and the stop tests on the device
         (csrc/vec.cu cbct_cgls_scalars): no host round trip inside, one synchronisation at the end,
@@ -574,21 +591,6 @@ class CglsRun:
         op = self.op
         return SolverReport(_final_volume(op, self.chain.x_of(self.x), self.b.data), self.i, self.nb,
                             self.history, getattr(op, "workers", 1), self.breakdown)
-
-
-def _nvtx(name):
-    """NVTX range around a public solver call (the kernels inside carry the C library's ranges:
-    cbct_project / cbct_backproject / cbct_normal_diagonal)."""
-    def deco(fn):
-        @functools.wraps(fn)
-        def wrapped(*args, **kwargs):
-            torch.cuda.nvtx.range_push(name)
-            try:
-                return fn(*args, **kwargs)
-            finally:
-                torch.cuda.nvtx.range_pop()
-        return wrapped
-    return deco
 
 
 @_nvtx("cbct_cgls")
@@ -672,6 +674,7 @@ class LsqrRun:
     def should_continue(self) -> bool:
         return not self.done and self.updates < self.cfg.max_iterations + 1
 
+    @_nvtx("cbct_lsqr_iteration")
     def step(self) -> None:
         """One bidiagonalisation step + Givens update + record (solvers.py:427-458)."""
         dev, chain, u, v = self.dev, self.chain, self.u, self.v
@@ -747,6 +750,7 @@ class LsqrRun:
         op.reduce_to(dev.nblocks(self.v.numel()), S[10:11])
         call("cbct_lsqr_scalars", _p(S), 2, st())
 
+    @_nvtx("cbct_lsqr_device_iterations")
     def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
         """Up to k LSQR iterations with the scalars on the device: one A, one A^T and two fused
         vector passes each (include/cbct.h cbct_lsqr_*), no host round trip inside; ``graph`` replays
@@ -892,6 +896,7 @@ class ClassicalRun:
         err = self.cfg.rel_discrepancy_tol
         return (err == 0.0 or self.e > err) and self.i < self.cfg.max_iterations
 
+    @_nvtx("cbct_classical_iteration")
     def step(self) -> None:
         dev, chain = self.dev, self.chain
         dev.mul(self.resid, self.inv_row, self.weighted)
@@ -920,6 +925,7 @@ class ClassicalRun:
         host loop's values (same kernels' arithmetic and reduction grids)."""
         return self.chain._fused and not self.dev.f64 and self.cfg.true_discrepancy_every <= 0
 
+    @_nvtx("cbct_classical_device_iterations")
     def run_device(self, k: int, graph: bool = False, collect: bool = True) -> None:
         if k <= 0 or not self.should_continue():
             return
