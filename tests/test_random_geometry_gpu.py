@@ -107,3 +107,39 @@ def test_random_geometry_f64_path(seed):
     assert max_rel(got, want) <= 1e-13, (seed, max_rel(got, want))
     got, want = op.normal_diagonal().data, ref.normal_diagonal()
     assert max_rel(got, want) <= 1e-13, (seed, max_rel(got, want))
+
+
+@pytest.mark.parametrize("case", ["nv2048", "nz2048", "nu1_one_view", "thin_slab_wide_det"])
+def test_size_limits_against_oracle(case):
+    """The largest detector height and volume depth the plan accepts (nv, nz <= 2048: four rays / voxels
+    per thread), a single detector column in a single view, and a one-slice volume under a wide
+    detector: A, A^T and diag(A^T A) against the oracle."""
+    import paper_2110_13526_b200 as P
+    from paper_2110_13526_b200.operator import CbctOperator, ProjectionStack
+    from paper_2110_13526_b200.phantom import Volume
+
+    if case == "nv2048":
+        vg = P.VolumeGeometry(12, 10, 40, (2.0, 2.0, 2.0))
+        det = P.DetectorGeometry(16, 2048, (2.0, 0.07))
+        tr = P.make_circular_trajectory(400.0, 700.0, 2, 0.3, 1.0, det)
+    elif case == "nz2048":
+        vg = P.VolumeGeometry(6, 7, 2048, (2.0, 2.0, 0.05))
+        det = P.DetectorGeometry(20, 300, (1.5, 0.6))
+        tr = P.make_circular_trajectory(400.0, 700.0, 2, 0.3, 1.0, det)
+    elif case == "nu1_one_view":
+        vg = P.VolumeGeometry(30, 30, 30, (1.0, 1.0, 1.0), (0.4, -0.3, 0.2))
+        det = P.DetectorGeometry(1, 64, (1.0, 1.0), (0.3, 0.0))
+        tr = P.make_circular_trajectory(300.0, 500.0, 1, 0.7, 0.0, det)
+    else:
+        vg = P.VolumeGeometry(50, 40, 1, (1.0, 1.0, 1.0))
+        det = P.DetectorGeometry(120, 101, (0.8, 0.8))
+        tr = P.make_circular_trajectory(300.0, 500.0, 3, 0.0, 2.0, det)
+    op, ref = CbctOperator(vg, tr), O.OracleOperator(vg, tr)
+    x = np.random.default_rng(5).random(op.n).astype(np.float32).astype(np.float64)
+    y = np.random.default_rng(6).standard_normal(op.m).astype(np.float32).astype(np.float64)
+    got, want = op.project(Volume(vg, x)).data, ref.project(x)
+    assert max_rel(got, want) <= TOL, (case, "A", max_rel(got, want))
+    got, want = op.backproject(ProjectionStack(tr, y)).data, ref.backproject(y)
+    assert max_rel(got, want) <= TOL, (case, "A^T", max_rel(got, want))
+    got, want = op.normal_diagonal().data, ref.normal_diagonal()
+    assert max_rel(got, want) <= TOL, (case, "normal_diagonal", max_rel(got, want))
