@@ -1,6 +1,7 @@
 """Operator parity at a FULL BASELINE configuration (not a subset) against the fp64 oracle.
 
 python tools/full_parity.py [cfg] > profiles/full_parity_config{cfg}.json
+(SKIP_F64=1 skips the fp64 path, SKIP_AT=1 stops after A: config 5's oracle A^T takes over 40 minutes)
 
 A x (phantom + uniform noise), A^T y (standard normal) and diag(A^T A) from the fp32 fast path, and A x from
 the fp64 path (bitwise check), against oracle/ (the C restatement of operator.py, all host threads).  The
@@ -49,6 +50,10 @@ if os.environ.get("SKIP_F64") is None:
     out["A_f64"] = cmp(got64, want)
     del op64, got64
 del want
+print(json.dumps(out), file=sys.stderr, flush=True)  # partial results (long oracle runs)
+if os.environ.get("SKIP_AT") is not None:  # config 5: the oracle's A^T alone takes over 40 minutes
+    print(json.dumps(out, indent=1))
+    sys.exit(0)
 op = P.CbctOperator(vg, tr)
 t = time.perf_counter()
 want = ref.backproject(y)
