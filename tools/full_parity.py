@@ -59,6 +59,10 @@ t = time.perf_counter()
 want = ref.backproject(y)
 out["oracle_AT_s"] = time.perf_counter() - t
 out["AT_f32"] = cmp(op.backproject(P.ProjectionStack(tr, y)).data, want)
+if os.environ.get("SKIP_F64") is None:
+    op64 = P.CbctOperator(vg, tr, precision="f64")
+    out["AT_f64"] = cmp(op64.backproject(P.ProjectionStack(tr, y)).data, want)
+    del op64
 del want
 t = time.perf_counter()
 want = ref.normal_diagonal()
