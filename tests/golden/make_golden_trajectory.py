@@ -4,7 +4,7 @@ reproducibility floor, at BASELINE configs 2 and 3/4 (subset).
 Run in the build container only (imports the reference from ``baseline/_ref/pkg`` like
 make_golden.py; ~1.5 h on 8 cores):
 
-    NUMBA_NUM_THREADS=8 python tests/golden/make_golden_trajectory.py [check] [subset] [config2]
+    NUMBA_NUM_THREADS=8 python tests/golden/make_golden_trajectory.py [check] [subset] [config2] [config2_lsqrj]
 
 Why: CGLS and LSQR in floating point lose orthogonality once the first Ritz values
 converge, and from then on any rounding difference grows roughly geometrically until it
@@ -162,7 +162,7 @@ def check():
     print("check: restated cgls / lsqr are bitwise equal to the reference")
 
 
-def _trajectories(name, vg, tr, lsqr_too):
+def _trajectories(name, vg, tr, lsqr_too, cgls_too=True):
     from cbctkit.operator import CbctOperator
 
     _, b = _problem(vg, tr)
@@ -171,9 +171,10 @@ def _trajectories(name, vg, tr, lsqr_too):
                snaps=np.array(SNAPS))
     for w in (8, 5):
         op = CbctOperator(vg, tr, workers=w)
-        t = time.perf_counter()
-        _store(out, f"cgls_w{w}", *cgls_snapshots(op, b, 40, SNAPS))
-        print(f"  cgls w={w}: {time.perf_counter() - t:.0f} s", flush=True)
+        if cgls_too:
+            t = time.perf_counter()
+            _store(out, f"cgls_w{w}", *cgls_snapshots(op, b, 40, SNAPS))
+            print(f"  cgls w={w}: {time.perf_counter() - t:.0f} s", flush=True)
         if lsqr_too:
             t = time.perf_counter()
             _store(out, f"lsqrj_w{w}", *lsqr_snapshots(op, b, 40, SNAPS, True))
@@ -191,6 +192,12 @@ def config2():
     _trajectories("config2", vg, tr, False)
 
 
+def config2_lsqrj():
+    """LSQR + Jacobi (config 4's solver) on BASELINE config 2 in full (~1 h on 8 cores)."""
+    vg, tr = _geometry(256, 360, 512, 384)
+    _trajectories("config2_lsqrj", vg, tr, True, cgls_too=False)
+
+
 def main(argv):
     if argv[:1] == ["compact"]:
         for name in argv[1:]:
@@ -199,9 +206,9 @@ def main(argv):
     _import_reference()
     for w in argv or ["check", "subset", "config2"]:
         print(w, flush=True)
-        {"check": check, "subset": subset, "config2": config2}[w]()
+        {"check": check, "subset": subset, "config2": config2, "config2_lsqrj": config2_lsqrj}[w]()
         if w != "check":
-            compact("config34_subset" if w == "subset" else "config2")
+            compact({"subset": "config34_subset"}.get(w, w))
 
 
 def compact(name):
