@@ -216,8 +216,8 @@ def test_config2_lsqr_jacobi40_full(precision):
     """LSQR + Jacobi (config 4's solver, solvers.py:158-193, 361-459) on BASELINE config 2 in full,
     against the reference's own run (tests/golden/make_golden_trajectory.py config2_lsqrj).
 
-    fp64 path: every history record through K = 30 to 1e-12 and the iterate after 20 to 1e-9
-    (measured 5.6e-14 / 8.5e-13); after 40, where the recurrence has left its rounding-stable phase
+    fp64 path: every history record through K = 30 to 1e-12 and the iterate after 20 to the
+    fp32-stored golden's resolution (measured 5.6e-14 / 8.5e-13 against the fp64 samples); after 40, where the recurrence has left its rounding-stable phase
     (ours: 2e-10 at K = 30, 1.1e-3 at K = 40; the reference's own floor, workers 5 vs 8: 2e-13 and
     1.5e-6), within LSQR40_F64_BAR of the reference's -- 10% above the north-star 1e-3, a known gap.
     fp32 path: after 10 iterations the history to 1e-6 (1.4e-7) and the iterate to 1e-3 on every voxel
@@ -243,7 +243,8 @@ def test_config2_lsqr_jacobi40_full(precision):
     if precision == "f64":
         rep, h = _solve(op, tr, b, "lsqr", 20, jacobi_precondition=True)
         assert float(np.abs(h / t["lsqrj_w8_hist"][:21] - 1.0).max()) <= 1e-12
-        assert rel_l2(rep.final_x.data[::st], t["lsqrj_w8_x20_sample"]) <= 1e-9
+        # the golden samples are stored in fp32 (6e-8 per voxel); measured 8.5e-13 against the fp64 samples
+        assert rel_l2(rep.final_x.data[::st], t["lsqrj_w8_x20_sample"]) <= 2e-7
         rep, h = _solve(op, tr, b, "lsqr", 40, jacobi_precondition=True)
         assert float(np.abs(h[:31] / t["lsqrj_w8_hist"][:31] - 1.0).max()) <= 1e-12
         rel = rel_l2(rep.final_x.data[::st], t["lsqrj_w8_x40_sample"])
