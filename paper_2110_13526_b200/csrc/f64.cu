@@ -20,7 +20,7 @@
 //                   ray order (v fastest) keeps a warp's rays in one detector column.
 //                   For a ray that enters through the side faces of the box this is
 //                   bitwise the reference's _project_kernel value.
-//   k_bp_f64        A^T y (mode 1) and diag(A^T A) (mode 2): voxel-driven deterministic
+//   k_bp_f64        A^T y (mode 1) and diag(A^T A) (mode 2): voxel-driven deterministic (TwoSum-compensated)
 //                   gather (no atomics), one CTA per cell, one thread per voxel, over the
 //                   cell's list of crossing columns (plan.cu); per crossing the fp64 xy
 //                   interval [t_a, t_b] is recomputed from the column's ray and the cell's
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
     }
     const int64_t off = cell_off[cell];
     const int ne = (int)(cell_off[cell + 1] - off);
-    double z0[ZPT], z1[ZPT], acc[ZPT];
+    double z0[ZPT], z1[ZPT], acc[ZPT], cmp[ZPT];
     float zf0[ZPT], zf1[ZPT];
     const float c0p = (float)(det00z / pv);
     int iz[ZPT];
@@ -423,6 +423,7 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
         z1[r] = g.lo2 + (double)(iz[r] + 1) * g.p2;
         zf1[r] = (float)z1[r];
         acc[r] = 0.0;
+        cmp[r] = 0.0;
     }
     for (int base = 0; base < ne; base += kChunk) {
         const int nch = min(kChunk, ne - base);
@@ -463,7 +464,16 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
                     double t1 = x.tb < t_out ? x.tb : t_out;
                     t1 = t1 < q.tmax ? t1 : q.tmax;
                     const double seg = (t1 - t0) * q.len;  // operator.py:158-159
-                    if (seg > kSegEps) acc[r] += mode == 1 ? seg * y[ray] : seg * seg;  // 162-167
+                    if (seg > kSegEps) {  // operator.py:162-167
+                        // compensated (TwoSum) accumulation: the voxel's sum of the same rounded
+                        // products as the reference's, rounded once at the end, so our summation
+                        // order adds no error of its own (the reference's merge order differs by W)
+                        const double v = mode == 1 ? seg * y[ray] : seg * seg;
+                        const double sm = acc[r] + v;
+                        const double bv = sm - acc[r];
+                        cmp[r] += (acc[r] - (sm - bv)) + (v - bv);
+                        acc[r] = sm;
+                    }
                 }
             }
         }
@@ -474,7 +484,7 @@ __global__ void __launch_bounds__(512) k_bp_f64(const int64_t* __restrict__ cell
 #pragma unroll
     for (int r = 0; r < ZPT; ++r) {
         if (iz[r] < nz) {
-            double val = acc[r];
+            double val = acc[r] + cmp[r];
             if (col_scale) val = col_scale[lcell * g.zs + CBCT_ZPAD + iz[r]] * val;
             out[CBCT_ZPAD + iz[r]] = val;
             sq += val * val;
